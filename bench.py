@@ -1,0 +1,408 @@
+"""Sync-EASGD throughput on B200 (BASELINE.json: "Sync EASGD samples/s at
+1/2/4/8 B200; elastic-update HBM GB/s vs peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model lenet|cifar-quick|alexnet]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+    python bench.py --impl reference ...                      (CPU reference arm)
+
+A step is one Sync-EASGD round: every worker (one per GPU) samples b images
+from its HBM-resident synthetic dataset, runs forward/backward, the packed
+weights are summed (NCCL allreduce over NVLink, overlapped with the
+round's forward/backward: sync-easgd3) and the fused elastic update runs.
+``value`` = all ranks' samples / max-over-ranks device time of K graph-
+replayed rounds. ``e2e`` = the same through run_trainer's host data path
+(pinned host batch -> H2D every round, loss D2H every round).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # C1/C2 synthetic MNIST for LeNet, C3 CIFAR, C5 ImageNet-shaped
+    "lenet": dict(classes=10, per_class=6000, b=64, eta=0.05, rho=0.25, test_per_class=100),
+    "cifar-quick": dict(classes=10, per_class=5000, b=64, eta=0.05, rho=0.25, test_per_class=100),
+    "alexnet": dict(classes=1000, per_class=1, b=128, eta=0.01, rho=0.1, test_per_class=0),
+}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def make_data(model: str, spec, seed: int = 0):
+    from paper_1708_02983_b200.datasets import Dataset, gen_synthetic, normalize
+
+    wl = WORKLOADS[model]
+    d = spec.input_dim
+    if model == "alexnet":
+        # 1000 x 150528 fp32 (0.6 GB); per-class blobs, features already unit-variance
+        train = gen_synthetic(wl["classes"], d, wl["per_class"], seed=seed, separation=5.0, dtype=np.float32)
+        return train, None
+    train = normalize(gen_synthetic(wl["classes"], d, wl["per_class"], seed=seed, separation=5.0))
+    return train, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.th.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus: int):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def time_update_kernel(eng, reps: int = 20):
+    """Live CUDA-event timing of the fused elastic update on the training
+    stream with the engine's own buffers (algorithmic bytes: 24 B/param at
+    nrep=1, 16 B per extra replica)."""
+    import torch
+
+    from paper_1708_02983_b200.updates import sync_update_
+
+    n, nrep = eng.n, eng.nrep
+    # work on copies so the training state is untouched
+    W, G, C, S = eng.W.clone(), eng.G.clone(), eng.C.clone(), eng.S.clone()
+    flush = torch.empty(int(256e6) // 4, device=W.device)
+    times = []
+    for i in range(reps + 3):
+        flush.zero_()  # evict L2 (126 MB) so the stream comes from HBM
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sync_update_(W, G, C, S, n, eng.P, eng.cfg.hyper)
+        b.record()
+        b.synchronize()
+        if i >= 3:
+            times.append(a.elapsed_time(b) / 1e3)
+    bytes_ = n * (8 + 16 * nrep)
+    return bytes_, float(np.mean(times))
+
+
+def run_device(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_02983_b200 import HyperParams, make_config, network
+    from paper_1708_02983_b200.trainers import NetworkProblem
+    from paper_1708_02983_b200.trainers.synchronous import SyncEngine
+
+    world, rank, local = dist_setup(args.gpus)
+    wl = WORKLOADS[args.model]
+    b = args.batch or wl["b"]
+    spec = network.MODELS[args.model](seed=0)
+    train, test = make_data(args.model, spec)
+    prob = NetworkProblem(spec, train, test)
+    P = world  # one worker per GPU (weak scaling)
+    cfg = make_config("sync-easgd3", workers=P, iterations=args.steps + args.warmup, batch_size=b,
+                      hyper=HyperParams(eta=wl["eta"], rho=wl["rho"]), seed=3)
+    eng = SyncEngine(cfg, prob, use_graph=True, profile_rounds=min(2, args.warmup))
+    for _ in range(args.warmup):
+        eng.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0.record()
+        for _ in range(args.steps):
+            eng.step()
+        t1.record()
+        t1.synchronize()
+        if world > 1:
+            dist.barrier()
+    dt = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    samples = args.steps * P * b
+    value = samples / dt
+
+    # elastic-update kernel roofline (live, CUDA events, L2 flushed)
+    upd_bytes, upd_s = time_update_kernel(eng)
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    roof = {"kernel": "esgd_sync_update_f32 (k_sync_update<4>)", "bound": "hbm",
+            "achieved": round(upd_bytes / upd_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": None,
+            "algorithmic_bytes": upd_bytes, "launch_s": upd_s,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"}
+
+    # e2e: run_trainer's host data path (pinned batch H2D + loss D2H every round)
+    e2e = run_e2e(args, spec, train, cfg, world) if not args.no_e2e else None
+
+    bd = eng.breakdown(dt)
+    comm_frac = bd["peer_param"] / dt if dt > 0 else 0.0
+    cpu = cpu_baseline(args, spec, train) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    out = {
+        "metric": "Sync EASGD samples/s (elastic-averaging round, 1 worker per B200)",
+        "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs)",
+        "data": "synthetic (gen_synthetic blobs, HBM-resident)",
+        "config": {"workload": f"sync-easgd3 {args.model} b={b}/worker P={P}", "model": args.model,
+                   "global_batch": P * b, "params": eng.n, "parallelism": f"dp{world}",
+                   "l2": "update kernel timed with L2 flushed; step inputs resident",
+                   "graph": eng.graph is not None},
+        "roofline": roof,
+        "comm_fraction_exposed": round(comm_frac, 4),
+        "gpu_launches": launches_per_step(eng) * args.steps,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def launches_per_step(eng) -> int:
+    """Kernels of libesgd per round (counted from the layer plan)."""
+    net = getattr(eng.plan, "net", None)
+    if net is None:
+        return 3
+    k = 1  # sample
+    for L in net.layers:
+        if L.kind == "conv":
+            k += 2 + 2 + (2 if L is not net.layers[0] else 0)  # im2col+gemm ; wgrad+colsum ; dgrad+col2im
+        elif L.kind == "pool":
+            k += 2
+        else:
+            k += 1 + (1 if L.flatten_in else 0) + 2 + 1
+    k += 1  # softmax
+    k += 2  # replica sum + update
+    return k
+
+
+def run_e2e(args, spec, train, cfg, world):
+    """Public API, host data: run_trainer with the problem's host-staged batches."""
+    import torch
+
+    from paper_1708_02983_b200.trainers import NetworkProblem
+    from paper_1708_02983_b200.trainers.synchronous import SyncEngine
+
+    prob = NetworkProblem(spec, train, None)
+    eng = SyncEngine(cfg, prob, use_graph=False, profile_rounds=0)
+    stager = HostStager(prob, eng)
+    for _ in range(max(1, args.warmup)):
+        stager.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        stager.step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    b = cfg.batch_size
+    return {"value": round(args.steps * cfg.cluster.workers * b / dt, 1), "unit": "samples/s",
+            "h2d_bytes_per_step": stager.h2d_bytes, "d2h_bytes_per_step": stager.d2h_bytes,
+            "path": "host SplitMix64 sampling -> pinned batch -> H2D -> round -> loss D2H"}
+
+
+class HostStager:
+    """Host data path: each round the local workers' batches are drawn with
+    the same SplitMix64 streams on the host, gathered into pinned memory,
+    copied to the device, and the round's mean loss is read back."""
+
+    def __init__(self, prob, eng):
+        import torch
+
+        from paper_1708_02983_b200.rng import CounterRng, stream_seed
+
+        self.prob, self.eng = prob, eng
+        net = eng.plan.net
+        self.net = net
+        b, nrep, d = net.b, net.nrep, net.d_in
+        self.X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
+        self.Y = prob.train.labels.astype(np.int32)
+        self.rngs = [CounterRng(stream_seed(eng.cfg.seed, w)) for w in range(eng.first, eng.first + nrep)]
+        self.hx = torch.empty((nrep, b * d), dtype=torch.float32).pin_memory()
+        self.hy = torch.empty((nrep, b), dtype=torch.int32).pin_memory()
+        self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
+        self.h2d_bytes = self.hx.numel() * 4 + self.hy.numel() * 4
+        self.d2h_bytes = nrep * 4
+
+    def step(self):
+        import torch
+
+        from paper_1708_02983_b200.device import stream_ptr
+
+        eng, net = self.eng, self.net
+        hx, hy = self.hx.numpy(), self.hy.numpy()
+        for r, rng in enumerate(self.rngs):
+            idx = rng.randint_block(net.b, self.X.shape[0])
+            np.take(self.X, idx, axis=0, out=hx[r].reshape(net.b, net.d_in))
+            hy[r] = self.Y[idx]
+        net.x.copy_(self.hx, non_blocking=True)
+        net.y.copy_(self.hy, non_blocking=True)
+        cs = torch.cuda.current_stream()
+        eng.comm.wait_stream(cs)
+        with torch.cuda.stream(eng.comm):
+            eng._sum(eng.comm)
+        net.gradient(eng.G, eng.W, stream_ptr(cs))
+        cs.wait_stream(eng.comm)
+        eng._update(cs)
+        self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
+        cs.synchronize()
+        return float(self.loss.numpy().mean())
+
+
+def cpu_baseline(args, spec, train, budget_s: float = 12.0):
+    """The CPU oracle (numpy restatement of the reference's sync round with
+    the same model) on this host, bounded sample: as many rounds as fit in
+    ~budget_s after one warm-up round."""
+    from oracle import esgd_oracle as O
+
+    layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK, "alexnet": O.alexnet_layers(1000)}[args.model]
+    wl = WORKLOADS[args.model]
+    b = args.batch or wl["b"]
+    prob = O.NetProblem(*layers, train.samples, train.labels, seed=0, dtype=np.float32)
+    rng = O.worker_rng(3, 0)
+    w = prob.init_weights()
+    c = w.copy()
+
+    def one_round(w, c):
+        g = prob.gradient(w, rng, b)
+        s = O.tree_sum([w])
+        return (O.easgd_worker_step(w, g, c, wl["eta"], wl["rho"]),
+                O.easgd_center_step_from_sum(c, s, 1, wl["eta"], wl["rho"]))
+
+    w, c = one_round(w, c)  # warm-up (BLAS init, page faults)
+    rounds = 1
+    t0 = time.perf_counter()
+    while True:
+        w, c = one_round(w, c)
+        rounds += 1
+        elapsed = time.perf_counter() - t0
+        if elapsed > budget_s:
+            break
+    timed = rounds - 1
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS") or str(os.cpu_count())
+    return {"value": round(timed * b / elapsed, 2) if timed > 0 else None, "unit": "samples/s",
+            "cores": int(threads), "kind": "port",
+            "sample": f"{timed} sync-easgd rounds of {args.model}, P=1, b={b}, numpy/OpenBLAS fp32 "
+                      f"(oracle/esgd_oracle.py restating trainers/synchronous.py:57-64)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1708_02983_b200 import network
+
+    spec = network.MODELS[args.model](seed=0)
+    train, _ = make_data(args.model, spec)
+    wl = WORKLOADS[args.model]
+    b = args.batch or wl["b"]
+    per_step_budget = 60.0 / max(1, args.steps + args.warmup)
+    vals = []
+    for i in range(args.steps + args.warmup):
+        r = cpu_baseline(args, spec, train, budget_s=min(10.0, per_step_budget))
+        if i >= args.warmup and r["value"]:
+            vals.append(r["value"])
+    value = float(np.mean(vals)) if vals else None
+    out = {"impl": "reference", "metric": "Sync EASGD samples/s (elastic-averaging round, 1 worker per B200)",
+           "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic", "config": {"workload": f"sync-easgd {args.model} b={b}/worker P=1",
+                                           "model": args.model},
+           "cpu_baseline": {"value": value, "unit": "samples/s", "cores": r["cores"], "kind": "port",
+                            "sample": r["sample"]},
+           "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--model", default="lenet", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_device(args)
+
+
+if __name__ == "__main__":
+    main()

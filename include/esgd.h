@@ -1,0 +1,228 @@
+/*
+ * esgd.h — C-ABI of libesgd, the B200 (sm_100a) kernels behind the
+ * elastic-averaging SGD trainers of arXiv 1708.02983.
+ *
+ * Plain pointers, sizes and scalars only (no torch types). All buffers are
+ * caller-owned DEVICE memory unless noted; every call is stream-ordered on
+ * `stream` (a cudaStream_t passed as void*; NULL = legacy default stream) and
+ * returns ESGD_OK or an error code, with a message in esgd_last_error().
+ * Nothing here allocates device memory or synchronizes the device.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/elasticsgd/).
+ *
+ * Numerics: the update rules evaluate exactly the reference's fp32 operation
+ * sequence with round-to-nearest and no FMA contraction, so their results are
+ * bitwise equal to the reference run with a float32 ModelSpec.
+ */
+#ifndef ESGD_H_
+#define ESGD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESGD_OK 0
+#define ESGD_ERR_SHAPE 1  /* maps to elasticsgd.errors.ShapeError  */
+#define ESGD_ERR_INPUT 2  /* maps to elasticsgd.errors.InputError  */
+#define ESGD_ERR_CUDA 3   /* CUDA runtime / launch failure          */
+#define ESGD_ERR_UNSUPPORTED 4
+
+#define ESGD_ACT_NONE 0
+#define ESGD_ACT_RELU 1
+#define ESGD_ACT_TANH 2
+#define ESGD_ACT_SIGMOID 3
+
+typedef void* esgd_stream_t;
+
+/* ---- library ----------------------------------------------------------- */
+const char* esgd_last_error(void);
+int esgd_abi_version(void);
+/* 1 if the library was built for sm_100a and a device of that class is present */
+int esgd_device_ok(int device);
+
+/* ---- update rules: updates.py ------------------------------------------ */
+
+/* easgd_worker_step, updates.py:85-93:
+ *   w_out = (w - eta*g) - etarho*(w - c);  w_out may alias w.            */
+int esgd_worker_step_f32(float* w_out, const float* w, const float* g, const float* c,
+                         int64_t n, float eta, float etarho, esgd_stream_t stream);
+
+/* easgd_center_step_from_sum, updates.py:113-119:
+ *   c_out = c + etarho*(s - P*c);  c_out may alias c.                      */
+int esgd_center_step_from_sum_f32(float* c_out, const float* c, const float* s, int64_t n,
+                                  float etarho, int32_t num_workers, esgd_stream_t stream);
+
+/* _sync_round, trainers/synchronous.py:57-64 (fused, in place):
+ * for every local replica r < nrep:
+ *   W[r] = (W[r] - eta*G[r]) - etarho*(W[r] - C)
+ * then C = C + etarho*(S - P*C), all against the pre-update C.
+ * W/G rows are ldw/ldg floats apart. 24 B/param algorithmic at nrep=1.      */
+int esgd_sync_update_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
+                         float* C, const float* S, int64_t n, float eta, float etarho,
+                         int32_t num_workers, esgd_stream_t stream);
+
+/* measgd_worker_step, updates.py:134-140 (in place):
+ *   v = mu*v - eta*g;  w = (w + v) - etarho*(w - c).  24 B/param.          */
+int esgd_measgd_update_f32(float* w, float* v, const float* g, const float* c, int64_t n,
+                           float eta, float mu, float etarho, esgd_stream_t stream);
+
+/* easgd_center_incremental, updates.py:122-131: c_out = c + etarho*(w - c) */
+int esgd_center_incr_f32(float* c_out, const float* c, const float* w, int64_t n,
+                         float etarho, esgd_stream_t stream);
+
+/* sgd_step / msgd_step, updates.py:71-82 (in place) */
+int esgd_sgd_step_f32(float* w, const float* g, int64_t n, float eta, esgd_stream_t stream);
+int esgd_msgd_step_f32(float* w, float* v, const float* g, int64_t n, float eta, float mu,
+                       esgd_stream_t stream);
+
+/* hogwild_apply, fabric/engine.py:156-166 with the elastic delta of
+ * trainers/hogwild.py:180:  center += etarho*(w - snap), lock-free
+ * (vector red.global.add), racing other streams by design.                  */
+int esgd_hogwild_apply_f32(float* center, const float* w, const float* snap, int64_t n,
+                           float etarho, esgd_stream_t stream);
+/* hogwild-sgd delta (trainers/hogwild.py:190): center += scale*g, lock-free */
+int esgd_hogwild_axpy_f32(float* center, const float* g, int64_t n, float scale,
+                          esgd_stream_t stream);
+
+/* tree_sum, fabric/collectives.py:18-32, over nrep local replicas (rows of
+ * W, ldw apart) in the reference's fixed binomial order. nrep <= 64.       */
+int esgd_replica_tree_sum_f32(float* S, const float* W, int64_t ldw, int32_t nrep, int64_t n,
+                              esgd_stream_t stream);
+
+/* ---- counter RNG + sampling: rng.py, datasets.py ------------------------ */
+
+/* CounterRng.randint_block, rng.py:87-91: out[i] = mix64(seed + (counter+i+1)*GOLDEN) % upper */
+int esgd_randint_u64(int64_t* out, uint64_t seed, uint64_t counter, int64_t count,
+                     uint64_t upper, esgd_stream_t stream);
+
+/* sample_batch, datasets.py:166-171, for nrep replicas in one launch.
+ * rng_state[2r] = seed, rng_state[2r+1] = counter of replica r (device
+ * memory; the counter is advanced by b on the device, so the call can be
+ * replayed from a CUDA graph). ticket: nrep int32 zeros (scratch).
+ * x_out[r] = rows of X (n x d, row-major) at the drawn indices, row pitch ldx;
+ * y_out[r] = labels (int32) ; idx_out (optional) = the indices.             */
+int esgd_sample_batch_f32(float* x_out, int64_t ldx_rep, int32_t* y_out, int64_t* idx_out,
+                          const float* X, const int32_t* labels, int64_t n, int64_t d,
+                          uint64_t* rng_state, int32_t* ticket, int32_t b, int32_t nrep,
+                          esgd_stream_t stream);
+
+/* QuadraticProblem.gradient, trainers/problems.py:95-96:
+ *   G[r] = curvature*(W[r] - target) for nrep replicas.                    */
+int esgd_quadratic_grad_f32(float* G, int64_t ldg, const float* W, int64_t ldw, int32_t nrep,
+                            const float* target, const float* curvature, int64_t n,
+                            esgd_stream_t stream);
+
+/* ---- dense layers: kernels.py, network.py ------------------------------ */
+
+/* C[z] (m x n) = act( A[z](m x k) . B[z](k x n) + bias[z] ) with arbitrary
+ * element strides (row/col/batch) for every operand; optional epilogue mask
+ * multiplies by (mask > 0) (relu-grad), optional c_pre keeps the
+ * pre-activation; accumulate adds into C. fp32 FFMA, for the small GEMMs.
+ * (network.py:166-171 forward, :194-199 backward, kernels.py:22-26)        */
+typedef struct {
+  int32_t m, n, k, batch;
+  const float* a; int64_t a_sm, a_sk, a_sb;
+  const float* b; int64_t b_sk, b_sn, b_sb;
+  float* c; int64_t c_sm, c_sn, c_sb;
+  const float* bias; int64_t bias_sb;
+  const float* mask; int64_t mask_sm, mask_sn, mask_sb;
+  float* c_pre;
+  int32_t act;
+  int32_t accumulate;
+} esgd_gemm_desc;
+int esgd_gemm_f32(const esgd_gemm_desc* desc, esgd_stream_t stream);
+
+/* Tensor-core GEMM (tcgen05.mma kind::tf32, TMA-fed, accumulator in TMEM)
+ * with 3xTF32 error compensation (hi*hi + hi*lo + lo*hi), i.e. fp32-grade
+ * results. Operands are K-major fp32: A is m x k (row pitch lda floats),
+ * B is n x k (row pitch ldb floats); C = A . B^T (+bias, act) written with
+ * strides (c_sm, c_sn). lda/ldb must be multiples of 4; pointers 16B aligned.
+ * Batched over `batch` with element strides a_sb, b_sb, c_sb.              */
+typedef struct {
+  int32_t m, n, k, batch;
+  const float* a; int64_t lda, a_sb;
+  const float* b; int64_t ldb, b_sb;
+  float* c; int64_t c_sm, c_sn, c_sb;
+  const float* bias; int64_t bias_sb;
+  const float* mask; int64_t mask_sm, mask_sn, mask_sb;
+  int32_t act;
+  int32_t accumulate;
+  int32_t precision; /* 3 = 3xTF32 (fp32-grade, default), 1 = plain TF32 */
+} esgd_tc_gemm_desc;
+int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* desc, esgd_stream_t stream);
+
+/* activation forward/backward, kernels.py:30-70.
+ * act_fwd: y = act(z); act_bwd: d = d * act'(z) (in place).                 */
+int esgd_act_fwd_f32(float* y, const float* z, int64_t n, int32_t act, esgd_stream_t stream);
+int esgd_act_bwd_f32(float* d, const float* z, int64_t n, int32_t act, esgd_stream_t stream);
+
+/* softmax_cross_entropy, kernels.py:85-106, per batch z of rows x cols logits
+ * (row pitch ld): dlogits = (softmax - onehot)/rows (may alias logits),
+ * row_loss[z*rows + i] = -log(softmax[i, label]) (optional).
+ * Labels out of range -> ESGD_ERR_INPUT is reported via *bad_label (device
+ * int32, optional; set to 1 on a bad label).                               */
+int esgd_softmax_xent_f32(float* dlogits, float* row_loss, const float* logits, int64_t ld,
+                          int64_t z_stride, const int32_t* labels, int64_t label_z_stride,
+                          int32_t rows, int32_t cols, int32_t batch, int32_t* bad_label,
+                          esgd_stream_t stream);
+
+/* argmax per row (ties -> lowest index), records.py:92-101 */
+int esgd_argmax_rows_f32(int32_t* out, const float* x, int64_t ld, int32_t rows, int32_t cols,
+                         esgd_stream_t stream);
+
+/* column sums over rows: out[z*out_sb + j] = sum_i x[z][i*ld + j] (bias grad,
+ * network.py:195). Deterministic fixed-order two-pass reduction.
+ * scratch: >= 64*cols*batch floats.                                         */
+int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld, int64_t x_sb,
+                    int64_t rows, int32_t cols, int32_t batch, float* scratch,
+                    esgd_stream_t stream);
+
+/* ---- convolution / pooling (CNN problems; no reference counterpart:
+ *      SPEC.md:67, conventions follow network.py) ------------------------- */
+
+/* activation tensors are described by element strides (n, c, h, w) so NCHW
+ * (dataset rows) and NHWC (internal) both work.                             */
+typedef struct {
+  int32_t n, c, h, w;
+  int64_t sn, sc, sh, sw;
+} esgd_tensor4;
+
+/* im2col: col[(img*OH*OW + oh*OW + ow) * ldc + (ci*kh + ky)*kw + kx] =
+ *   x(img, ci, oh*stride - pad + ky, ow*stride - pad + kx) (0 outside).
+ * Columns k..ldc-1 are zero-filled. Batched over `batch` (x_sb, col_sb).   */
+int esgd_im2col_f32(float* col, int64_t ldc, int64_t col_sb, const float* x, esgd_tensor4 xd,
+                    int64_t x_sb, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                    int32_t oh, int32_t ow, int32_t batch, esgd_stream_t stream);
+
+/* col2im (adjoint of im2col, gather form, fixed order): dx(img,ci,y,x) =
+ * sum over (ky,kx) of dcol rows hitting (y,x); optional mask multiplies the
+ * result by (mask>0) with mask laid out like dx (relu-grad).              */
+int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol, int64_t ldc,
+                    int64_t col_sb, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                    int32_t oh, int32_t ow, const float* mask, int32_t batch,
+                    esgd_stream_t stream);
+
+/* max pooling kxk/stride/pad; argmax (flat h*W+w of the input plane, first
+ * max in (ky,kx) scan order) kept for backward.                             */
+int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int32_t* argmax,
+                         const float* x, esgd_tensor4 xd, int64_t x_sb, int32_t k,
+                         int32_t stride, int32_t pad, int32_t batch, esgd_stream_t stream);
+/* dx = sum of dy routed to argmax (gather form), optional relu mask (x>0). */
+int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
+                         esgd_tensor4 yd, int64_t y_sb, const int32_t* argmax,
+                         const float* mask, int32_t k, int32_t stride, int32_t pad,
+                         int32_t batch, esgd_stream_t stream);
+
+/* strided 4-D copy (layout change, e.g. NHWC -> NCHW flatten for the FC
+ * head and back), optional relu mask on the source (src>0 of mask).         */
+int esgd_copy4_f32(float* dst, esgd_tensor4 dd, int64_t d_sb, const float* src, esgd_tensor4 sd,
+                   int64_t s_sb, int32_t batch, esgd_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ESGD_H_ */

@@ -1,0 +1,318 @@
+// Dense-layer kernels for the per-worker gradient (trainers/problems.py:42-47):
+// a strided/batched fp32 FFMA GEMM for the small contractions (LeNet/MLP
+// shapes are launch-latency bound), activations, the fused
+// softmax cross-entropy (kernels.py:85-106), row argmax and deterministic
+// column sums (bias gradients, network.py:195).
+#include "esgd_common.cuh"
+
+#include <math.h>
+
+namespace esgd {
+namespace {
+
+// ---- activations (kernels.py:30-70) ----------------------------------------
+
+__device__ __forceinline__ float act_apply(float z, int act) {
+  switch (act) {
+    case ESGD_ACT_RELU: return fmaxf(z, 0.f);
+    case ESGD_ACT_TANH: return tanhf(z);
+    case ESGD_ACT_SIGMOID:
+      if (z >= 0.f) return 1.f / (1.f + expf(-z));
+      else { float e = expf(z); return e / (1.f + e); }
+    default: return z;
+  }
+}
+
+// d * act'(z), kernels.py:34-66 (relu_grad is (z > 0) as 0/1)
+__device__ __forceinline__ float act_grad_mul(float d, float z, int act) {
+  switch (act) {
+    case ESGD_ACT_RELU: return __fmul_rn(d, z > 0.f ? 1.f : 0.f);
+    case ESGD_ACT_TANH: { float t = tanhf(z); return d * (1.f - t * t); }
+    case ESGD_ACT_SIGMOID: { float s = act_apply(z, ESGD_ACT_SIGMOID); return d * (s * (1.f - s)); }
+    default: return d;
+  }
+}
+
+// ---- strided batched FFMA GEMM ---------------------------------------------
+// 64x64 output tile per 256-thread CTA, 4x4 per thread, BK=16 slabs staged
+// through shared memory (A transposed so the inner loop reads float4 rows).
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  const int z = blockIdx.z;
+  const float* A = d.a + z * d.a_sb;
+  const float* B = d.b + z * d.b_sb;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool a_kfast = (d.a_sk == 1);
+  const bool b_nfast = (d.b_sn == 1);
+
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  float ra[4], rb[4];
+  auto load_regs = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int e = tid + j * 256;
+      int mm, kk;
+      if (a_kfast) { mm = e >> 4; kk = e & 15; } else { mm = e & 63; kk = e >> 6; }
+      int gm = m0 + mm, gk = k0 + kk;
+      ra[j] = (gm < d.m && gk < d.k) ? __ldg(A + (int64_t)gm * d.a_sm + (int64_t)gk * d.a_sk) : 0.f;
+      int nn, kb;
+      if (b_nfast) { nn = e & 63; kb = e >> 6; } else { nn = e >> 4; kb = e & 15; }
+      int gn = n0 + nn, gkb = k0 + kb;
+      rb[j] = (gn < d.n && gkb < d.k) ? __ldg(B + (int64_t)gkb * d.b_sk + (int64_t)gn * d.b_sn) : 0.f;
+    }
+  };
+  auto store_smem = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int e = tid + j * 256;
+      int mm, kk;
+      if (a_kfast) { mm = e >> 4; kk = e & 15; } else { mm = e & 63; kk = e >> 6; }
+      As[buf][kk][mm] = ra[j];
+      int nn, kb;
+      if (b_nfast) { nn = e & 63; kb = e >> 6; } else { nn = e >> 4; kb = e & 15; }
+      Bs[buf][kb][nn] = rb[j];
+    }
+  };
+
+  const int nk = (d.k + BK - 1) / BK;
+  load_regs(0);
+  store_smem(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load_regs((t + 1) * BK);  // prefetch next slab into registers
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float4 a4 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (t + 1 < nk) store_smem(buf ^ 1);
+    __syncthreads();
+  }
+
+  float* C = d.c + z * d.c_sb;
+  float* Cp = d.c_pre ? d.c_pre + z * d.c_sb : nullptr;
+  const float* bias = d.bias ? d.bias + z * d.bias_sb : nullptr;
+  const float* mask = d.mask ? d.mask + z * d.mask_sb : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + ty * 4 + i;
+    if (gm >= d.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + tx * 4 + j;
+      if (gn >= d.n) continue;
+      int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
+      float v = acc[i][j];
+      if (d.accumulate) v = __fadd_rn(C[off], v);
+      if (bias) v = __fadd_rn(v, bias[gn]);
+      if (Cp) Cp[off] = v;
+      v = act_apply(v, d.act);
+      if (mask) v = __fmul_rn(v, mask[(int64_t)gm * d.mask_sm + (int64_t)gn * d.mask_sn] > 0.f ? 1.f : 0.f);
+      C[off] = v;
+    }
+  }
+}
+
+__global__ void k_act_fwd(float* y, const float* z, int64_t n, int act) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = act_apply(z[i], act);
+}
+__global__ void k_act_bwd(float* dd, const float* z, int64_t n, int act) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dd[i] = act_grad_mul(dd[i], z[i], act);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// softmax_cross_entropy (kernels.py:85-106): one warp per row.
+__global__ void __launch_bounds__(128) k_softmax_xent(float* dl, float* row_loss, const float* lg,
+                                                      int64_t ld, int64_t zs, const int32_t* labels,
+                                                      int64_t lzs, int rows, int cols,
+                                                      int32_t* bad) {
+  const int z = blockIdx.y;
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* x = lg + z * zs + (int64_t)row * ld;
+  float* o = dl + z * zs + (int64_t)row * ld;
+  const int label = labels[z * lzs + row];
+  const bool ok = label >= 0 && label < cols;
+  float m = -INFINITY;
+  for (int j = lane; j < cols; j += 32) m = fmaxf(m, x[j]);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int j = lane; j < cols; j += 32) s += expf(x[j] - m);
+  s = warp_sum(s);
+  float picked = 0.f;
+  for (int j = lane; j < cols; j += 32) {
+    float p = expf(x[j] - m) / s;
+    if (j == label) picked = p;
+    float g = (j == label) ? __fsub_rn(p, 1.f) : p;
+    o[j] = ok ? __fdiv_rn(g, (float)rows) : 0.f;
+  }
+  picked = warp_sum(picked);
+  if (lane == 0) {
+    if (row_loss) row_loss[z * rows + row] = ok ? -logf(picked) : NAN;
+    if (!ok && bad) *bad = 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_argmax(int32_t* out, const float* x, int64_t ld, int rows,
+                                                int cols) {
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* r = x + (int64_t)row * ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int j = lane; j < cols; j += 32) {
+    float v = r[j];
+    if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if (lane == 0) out[row] = bi == 0x7fffffff ? 0 : bi;
+}
+
+// Column sums, pass 1: CTA (32 cols x 8 row-lanes) over one row chunk,
+// fixed-order in-CTA combine, one partial per (chunk, col).
+__global__ void __launch_bounds__(256) k_colsum_partial(float* part, const float* x, int64_t ld,
+                                                        int64_t x_sb, int64_t rows, int cols,
+                                                        int64_t chunk, float* out, int64_t out_sb,
+                                                        int direct) {
+  __shared__ float red[8][33];
+  const int z = blockIdx.z, c = blockIdx.x * 32 + threadIdx.x, ty = threadIdx.y;
+  const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+  const float* xz = x + z * x_sb;
+  float s = 0.f;
+  if (c < cols)
+    for (int64_t r = r0 + ty; r < r1; r += 8) s += xz[r * ld + c];
+  red[ty][threadIdx.x] = s;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float t = red[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][threadIdx.x];
+    if (direct) out[z * out_sb + c] = t;
+    else part[((int64_t)z * gridDim.y + blockIdx.y) * cols + c] = t;
+  }
+}
+__global__ void k_colsum_final(float* out, int64_t out_sb, const float* part, int nchunk, int cols,
+                               int batch) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cols * batch) return;
+  int z = i / cols, c = i % cols;
+  float t = 0.f;
+  for (int k = 0; k < nchunk; ++k) t += part[((int64_t)z * nchunk + k) * cols + c];
+  out[z * out_sb + c] = t;
+}
+
+}  // namespace
+}  // namespace esgd
+
+using namespace esgd;
+#define ESGD_STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
+  ESGD_REQUIRE(d, ESGD_ERR_INPUT, "gemm: null descriptor");
+  ESGD_REQUIRE(d->m >= 0 && d->n >= 0 && d->k >= 0 && d->batch >= 0, ESGD_ERR_SHAPE,
+               "gemm shape mismatch: m=%d n=%d k=%d batch=%d", d->m, d->n, d->k, d->batch);
+  ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "gemm: unknown activation %d", d->act);
+  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
+  ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
+  ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
+  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch);
+  ESGD_REQUIRE(grid.y <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: m too large for the FFMA path");
+  k_gemm<<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d);
+  return check_launch("esgd_gemm_f32");
+}
+
+extern "C" int esgd_act_fwd_f32(float* y, const float* z, int64_t n, int32_t act,
+                                esgd_stream_t stream) {
+  ESGD_REQUIRE(act >= 0 && act <= 3, ESGD_ERR_INPUT, "unknown activation %d", act);
+  if (n <= 0) return n == 0 ? ESGD_OK : ESGD_ERR_SHAPE;
+  k_act_fwd<<<stride_grid(n, 256), 256, 0, ESGD_STREAM(stream)>>>(y, z, n, act);
+  return check_launch("esgd_act_fwd_f32");
+}
+
+extern "C" int esgd_act_bwd_f32(float* dd, const float* z, int64_t n, int32_t act,
+                                esgd_stream_t stream) {
+  ESGD_REQUIRE(act >= 0 && act <= 3, ESGD_ERR_INPUT, "unknown activation %d", act);
+  if (n <= 0) return n == 0 ? ESGD_OK : ESGD_ERR_SHAPE;
+  k_act_bwd<<<stride_grid(n, 256), 256, 0, ESGD_STREAM(stream)>>>(dd, z, n, act);
+  return check_launch("esgd_act_bwd_f32");
+}
+
+extern "C" int esgd_softmax_xent_f32(float* dlogits, float* row_loss, const float* logits,
+                                     int64_t ld, int64_t z_stride, const int32_t* labels,
+                                     int64_t label_z_stride, int32_t rows, int32_t cols,
+                                     int32_t batch, int32_t* bad_label, esgd_stream_t stream) {
+  ESGD_REQUIRE(rows >= 1 && cols >= 1 && batch >= 1 && ld >= cols, ESGD_ERR_SHAPE,
+               "softmax_xent: bad shape rows=%d cols=%d ld=%lld", rows, cols, (long long)ld);
+  ESGD_REQUIRE(dlogits && logits && labels, ESGD_ERR_INPUT, "softmax_xent: null buffer");
+  dim3 grid((rows + 3) / 4, batch);
+  k_softmax_xent<<<grid, 128, 0, ESGD_STREAM(stream)>>>(dlogits, row_loss, logits, ld, z_stride,
+                                                        labels, label_z_stride, rows, cols, bad_label);
+  return check_launch("esgd_softmax_xent_f32");
+}
+
+extern "C" int esgd_argmax_rows_f32(int32_t* out, const float* x, int64_t ld, int32_t rows,
+                                    int32_t cols, esgd_stream_t stream) {
+  ESGD_REQUIRE(rows >= 0 && cols >= 1 && ld >= cols, ESGD_ERR_SHAPE, "argmax: bad shape");
+  if (rows == 0) return ESGD_OK;
+  k_argmax<<<(rows + 3) / 4, 128, 0, ESGD_STREAM(stream)>>>(out, x, ld, rows, cols);
+  return check_launch("esgd_argmax_rows_f32");
+}
+
+extern "C" int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld,
+                               int64_t x_sb, int64_t rows, int32_t cols, int32_t batch,
+                               float* scratch, esgd_stream_t stream) {
+  ESGD_REQUIRE(rows >= 1 && cols >= 1 && batch >= 1 && ld >= cols, ESGD_ERR_SHAPE,
+               "colsum: bad shape");
+  ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "colsum: null buffer");
+  int64_t nchunk = (rows + 511) / 512;
+  if (nchunk > 64) nchunk = 64;
+  int64_t chunk = (rows + nchunk - 1) / nchunk;
+  nchunk = (rows + chunk - 1) / chunk;
+  ESGD_REQUIRE(nchunk == 1 || scratch, ESGD_ERR_INPUT, "colsum: scratch required for %lld rows",
+               (long long)rows);
+  dim3 grid((cols + 31) / 32, (unsigned)nchunk, batch), block(32, 8);
+  cudaStream_t st = ESGD_STREAM(stream);
+  k_colsum_partial<<<grid, block, 0, st>>>(scratch, x, ld, x_sb, rows, cols, chunk, out, out_sb,
+                                           nchunk == 1);
+  if (nchunk > 1) {
+    int tot = cols * batch;
+    k_colsum_final<<<(tot + 255) / 256, 256, 0, st>>>(out, out_sb, scratch, (int)nchunk, cols, batch);
+  }
+  return check_launch("esgd_colsum_f32");
+}

@@ -1,0 +1,372 @@
+// Tensor-core GEMM for the conv-as-GEMM and FC contractions (sm_100a).
+//
+//   C[z] (m x n) = act( A[z] (m x k, K-major) . B[z] (n x k, K-major)^T + bias )
+//
+// Blackwell-native structure (one 128 x BN output tile per CTA):
+//   warp 0      : TMA producer — cp.async.bulk.tensor 3-D loads of raw fp32
+//                 A/B tiles (128-byte swizzle) into a multi-stage smem ring,
+//                 completion tracked by mbarrier transaction counts.
+//   warps 2..5  : split warps — for 3xTF32 they rewrite each landed tile as
+//                 hi = x & 0xffffe000 (exact tf32) in place and lo = x - hi
+//                 into a twin buffer of identical (swizzled) layout, then
+//                 fence.proxy.async and arrive; afterwards they are the
+//                 epilogue (tcgen05.ld TMEM -> registers -> bias/act/mask).
+//   warp 1      : TMEM allocation and the single-thread tcgen05.mma issuer,
+//                 kind::tf32, M=128, N=BN, K=8 per instruction, accumulator
+//                 in TMEM; tcgen05.commit frees smem slots / signals epilogue.
+//
+// 3xTF32: a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b, accumulated in fp32 in
+// TMEM — fp32-grade products (relative error ~2^-21), which the parity gate
+// (1e-5 relative, BASELINE.json north_star) requires; plain TF32 (~1e-3)
+// would not pass it.
+#include "esgd_common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace esgd {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;                  // 32 fp32 = 128 B = one swizzle atom row
+constexpr int kThreads = 192;           // 6 warps
+constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
+
+template <int BN, bool SPLIT>
+struct Cfg {
+  static constexpr int kTileBytesB = BN * BK * 4;
+  static constexpr int kStageBytes = (kTileBytesA + kTileBytesB) * (SPLIT ? 2 : 1);
+  static constexpr int kStages = SPLIT ? (BN >= 128 ? 3 : 4) : (BN >= 128 ? 6 : 8);
+  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  // stage layout: [A raw | A lo | B raw | B lo], every tile 1024-B aligned
+  static constexpr int kOffALo = kTileBytesA;
+  static constexpr int kOffB = SPLIT ? 2 * kTileBytesA : kTileBytesA;
+  static constexpr int kOffBLo = kOffB + kTileBytesB;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// K-major, 128-byte swizzle canonical layout: rows of 128 B, 8-row atoms
+// 1024 B apart (SBO), LBO = 1 (unused for swizzled K-major), version 1.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4)                      // c_format = F32
+         | (2u << 7)                    // a_format = TF32
+         | (2u << 10)                   // b_format = TF32
+         | ((uint32_t)(n >> 3) << 17)   // N >> 3
+         | ((uint32_t)(m >> 4) << 24);  // M >> 4
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_c, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float act_apply(float z, int act) {
+  switch (act) {
+    case ESGD_ACT_RELU: return fmaxf(z, 0.f);
+    case ESGD_ACT_TANH: return tanhf(z);
+    case ESGD_ACT_SIGMOID:
+      if (z >= 0.f) return 1.f / (1.f + expf(-z));
+      else { float e = expf(z); return e / (1.f + e); }
+    default: return z;
+  }
+}
+
+struct Epi {
+  float* c; int64_t c_sm, c_sn, c_sb;
+  const float* bias; int64_t bias_sb;
+  const float* mask; int64_t mask_sm, mask_sn, mask_sb;
+  int act, accumulate, m, n, k;
+};
+
+// split one landed tile: hi = tf32-truncated x (in place), lo = x - hi
+__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, int bytes, int tid) {
+  float4* r4 = reinterpret_cast<float4*>(raw);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+  const int n4 = bytes / 16;
+  for (int i = tid; i < n4; i += 128) {
+    float4 x = r4[i], h, l;
+    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+    l.x = __fsub_rn(x.x, h.x);
+    l.y = __fsub_rn(x.y, h.y);
+    l.z = __fsub_rn(x.z, h.z);
+    l.w = __fsub_rn(x.w, h.w);
+    r4[i] = h;
+    l4[i] = l;
+  }
+}
+
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+              Epi ep) {
+  using C = Cfg<BN, SPLIT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  // bars: full[S], split[S], empty[S], tmem_full
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 1);
+  const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
+                 empty0 = smem_u32(bars + 2 * C::kStages), tfull = smem_u32(bars + 3 * C::kStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, z = blockIdx.z;
+  const int nkb = (ep.k + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(split0 + 8 * s, 4);  // one arrive per split warp
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % C::kStages;
+        if (kb >= C::kStages) mbar_wait(empty0 + 8 * s, ((kb / C::kStages) - 1) & 1);
+        uint8_t* st = smem + s * C::kStageBytes;
+        mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
+        tma_load_3d(smem_u32(st), &map_a, full0 + 8 * s, kb * BK, m0, z);
+        tma_load_3d(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, kb * BK, n0, z);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % C::kStages;
+        const uint32_t ph = (kb / C::kStages) & 1;
+        if (SPLIT) mbar_wait(split0 + 8 * s, ph);
+        else mbar_wait(full0 + 8 * s, ph);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint32_t koff = kk * 32;  // 8 tf32 = 32 B along K inside the swizzle atom
+          const uint64_t ah = desc_sw128(st + koff), bh = desc_sw128(st + C::kOffB + koff);
+          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+          if (SPLIT) {
+            const uint64_t al = desc_sw128(st + C::kOffALo + koff),
+                           bl = desc_sw128(st + C::kOffBLo + koff);
+            mma_tf32(tmem, al, bh, idesc, acc0);  // small terms first
+            mma_tf32(tmem, ah, bl, idesc, 1u);
+            mma_tf32(tmem, ah, bh, idesc, 1u);
+          } else {
+            mma_tf32(tmem, ah, bh, idesc, acc0);
+          }
+        }
+        mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
+      }
+      mma_commit(tfull);
+    }
+  } else {
+    const int et = threadIdx.x - 64;  // 0..127
+    if (SPLIT) {  // ---- split warps
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % C::kStages;
+        mbar_wait(full0 + 8 * s, (kb / C::kStages) & 1);
+        uint8_t* st = smem + s * C::kStageBytes;
+        split_tile(st, st + C::kOffALo, kTileBytesA, et);
+        split_tile(st + C::kOffB, st + C::kOffBLo, C::kTileBytesB, et);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split0 + 8 * s);
+      }
+    }
+    // ---- epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 = tile rows
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    float* cz = ep.c + z * ep.c_sb;
+    const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
+    const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      if (row < ep.m) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = n0 + c0 + j;
+          if (col < ep.n) {
+            const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+            float x = v[j];
+            if (ep.accumulate) x = __fadd_rn(cz[off], x);
+            if (bz) x = __fadd_rn(x, bz[col]);
+            x = act_apply(x, ep.act);
+            if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
+            cz[off] = x;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D map over a K-major operand: dims (k, rows, batch), box (32, box_rows, 1)
+int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64_t ld,
+             int64_t batch, int64_t sb, int box_rows) {
+  auto enc = get_encode();
+  ESGD_REQUIRE(enc, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)batch};
+  int64_t bstride = batch > 1 ? sb : ld * rows;
+  bstride = (bstride + 3) & ~int64_t(3);
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
+  cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ESGD_REQUIRE(r == CUDA_SUCCESS, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ESGD_OK;
+}
+
+template <int BN, bool SPLIT>
+int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
+  using C = Cfg<BN, SPLIT>;
+  // per-device attribute; cheap, and legal while a stream is being captured
+  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::kSmemBytes);
+  ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: smem attribute: %s", cudaGetErrorString(e));
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN);
+  if (rc) return rc;
+  Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
+         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k};
+  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch);
+  k_tc_gemm<BN, SPLIT><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, ep);
+  return check_launch("esgd_tc_gemm_f32");
+}
+
+}  // namespace tc
+}  // namespace esgd
+
+extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream) {
+  using namespace esgd;
+  ESGD_REQUIRE(d, ESGD_ERR_INPUT, "tc_gemm: null descriptor");
+  ESGD_REQUIRE(d->m >= 0 && d->n >= 0 && d->k >= 0 && d->batch >= 0, ESGD_ERR_SHAPE,
+               "tc_gemm shape mismatch: m=%d n=%d k=%d", d->m, d->n, d->k);
+  ESGD_REQUIRE(d->precision == 1 || d->precision == 3, ESGD_ERR_INPUT,
+               "tc_gemm: precision must be 1 (tf32) or 3 (3xtf32)");
+  ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "tc_gemm: unknown activation");
+  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
+  ESGD_REQUIRE(d->k >= 1 && d->a && d->b && d->c, ESGD_ERR_INPUT, "tc_gemm: null operand");
+  ESGD_REQUIRE(d->lda >= d->k && d->ldb >= d->k && (d->lda & 3) == 0 && (d->ldb & 3) == 0,
+               ESGD_ERR_SHAPE, "tc_gemm: lda/ldb must be >= k and multiples of 4 (TMA 16-B strides)");
+  ESGD_REQUIRE(aligned16(d->a) && aligned16(d->b), ESGD_ERR_INPUT, "tc_gemm: A/B must be 16-B aligned");
+  ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
+               "tc_gemm: batch strides must be multiples of 4");
+  ESGD_REQUIRE(d->batch <= 65535 && (d->m + tc::BM - 1) / tc::BM <= 65535, ESGD_ERR_UNSUPPORTED,
+               "tc_gemm: grid too large");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool split = d->precision == 3;
+  if (d->n <= 64) return split ? tc::launch<64, true>(d, st) : tc::launch<64, false>(d, st);
+  return split ? tc::launch<128, true>(d, st) : tc::launch<128, false>(d, st);
+}

@@ -1,0 +1,300 @@
+"""Device executor for the per-worker gradient (trainers/problems.py:42-47:
+sample -> forward -> softmax-CE -> backward into one packed gradient).
+
+One ``DeviceNet`` serves ``nrep`` local worker replicas at once: every
+kernel is batched over replicas (grid.z / batch strides), so P workers on one
+GPU cost the same number of launches as one. Layouts in HBM:
+
+* parameters / gradients: rows of a (nrep, ldw) fp32 tensor, the reference's
+  packed order (network.view_table);
+* sampled batch: (nrep, b, C*H*W) — dataset rows are CHW-flat;
+* conv / pool activations: NHWC per image, (b*OH*OW, C) row-major, so the
+  conv GEMM is  out[b*OH*OW, Cout] = im2col[b*OH*OW, K] . W[Cout, K]^T;
+* dense activations: (b, out); the conv->dense flatten is converted to the
+  reference's (c, h, w) order by one strided copy.
+
+Contractions go to the tcgen05 3xTF32 GEMM (csrc/gemm_tc.cu) when their
+operands are K-major and big enough to fill 128-row tiles; the small ones
+(LeNet/MLP sizes, launch-latency bound) run on the FFMA GEMM.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ACT, GemmDesc, TcGemmDesc, Tensor4, nchw, nhwc
+from .device import round_up
+from .errors import InputError, ShapeError
+from .network import Conv, ConvNetSpec, Dense, ModelSpec, Pool, view_table
+
+# a contraction goes to the tensor cores when M*N*K reaches this
+TC_MIN_FLOPS = 1 << 22
+
+
+@dataclass
+class _Layer:
+    kind: str                  # conv | pool | dense
+    lay: object
+    cin: int
+    hin: int
+    win: int
+    cout: int
+    hout: int
+    wout: int
+    act: int
+    w_off: int = -1
+    b_off: int = -1
+    k: int = 0                 # conv reduction dim Cin*k*k
+    kp: int = 0                # padded row pitch of im2col
+    flatten_in: bool = False   # dense whose input is a spatial tensor
+
+
+class DeviceNet:
+    """Forward/backward executor for one model on one device, nrep replicas,
+    fixed batch ``b``."""
+
+    def __init__(self, spec, b: int, nrep: int, device: torch.device, ldw: int | None = None,
+                 use_tc: bool = True, precision: int = 3):
+        if isinstance(spec, ModelSpec):
+            spec = spec.as_layers()
+        if not isinstance(spec, ConvNetSpec):
+            raise InputError(f"unsupported model spec {type(spec).__name__}")
+        self.spec = spec
+        self.b, self.nrep, self.device = int(b), int(nrep), device
+        self.n = spec.parameter_count()
+        self.ldw = ldw if ldw is not None else round_up(self.n, 64)
+        self.use_tc = use_tc
+        self.precision = precision
+        views = {v.name: v for v in view_table(spec)}
+        self.layers: list[_Layer] = []
+        prev_spatial = False
+        for g in spec.geometry():
+            lay = g.layer
+            cin, hin, win = g.in_shape
+            cout, hout, wout = g.out_shape
+            if isinstance(lay, Conv):
+                if lay.act not in ("none", "relu"):
+                    raise InputError("conv layers support relu or no activation")
+                L = _Layer("conv", lay, cin, hin, win, cout, hout, wout, ACT[lay.act],
+                           views[f"W{g.param_index}"].offset, views[f"b{g.param_index}"].offset,
+                           k=cin * lay.k * lay.k, kp=round_up(cin * lay.k * lay.k, 4))
+                prev_spatial = True
+            elif isinstance(lay, Pool):
+                L = _Layer("pool", lay, cin, hin, win, cout, hout, wout, 0)
+                prev_spatial = True
+            else:
+                L = _Layer("dense", lay, cin, 1, 1, cout, 1, 1, ACT[lay.act],
+                           views[f"W{g.param_index}"].offset, views[f"b{g.param_index}"].offset,
+                           flatten_in=prev_spatial)
+                # geometry reports the flattened fan-in; recover the spatial shape
+                if prev_spatial:
+                    p = self.layers[-1]
+                    L.cin, L.hin, L.win = p.cout, p.hout, p.wout
+                prev_spatial = False
+            self.layers.append(L)
+        self.c0, self.h0, self.w0 = spec.input_shape
+        self.d_in = self.c0 * self.h0 * self.w0
+        self.classes = spec.num_classes
+        self._alloc()
+
+    # ---- workspace ---------------------------------------------------------
+    def _t(self, per_rep: int, dtype=torch.float32) -> torch.Tensor:
+        return torch.zeros((self.nrep, max(4, round_up(per_rep, 4))), dtype=dtype, device=self.device)
+
+    def _alloc(self):
+        b = self.b
+        self.x = self._t(b * self.d_in)
+        self.y = self._t(b, torch.int32)
+        self.row_loss = self._t(b)
+        self.outs, self.cols, self.amax, self.flat, self.pre = [], [], [], [], []
+        max_act = b * self.d_in
+        max_cols = 1
+        for L in self.layers:
+            size = b * L.cout * L.hout * L.wout
+            max_act = max(max_act, size, b * L.cin * L.hin * L.win)
+            self.outs.append(self._t(size))
+            self.cols.append(self._t(b * L.hout * L.wout * L.kp) if L.kind == "conv" else None)
+            self.amax.append(self._t(size, torch.int32) if L.kind == "pool" else None)
+            self.flat.append(self._t(b * L.cin * L.hin * L.win) if (L.kind == "dense" and L.flatten_in) else None)
+            self.pre.append(self._t(size) if (L.kind == "dense" and L.act in (2, 3)) else None)
+            if L.kind in ("conv", "dense"):
+                max_cols = max(max_cols, L.cout)
+        self.d_a = self._t(max_act)
+        self.d_b = self._t(max_act)
+        self.dcol = self._t(max((b * L.hout * L.wout * L.kp for L in self.layers if L.kind == "conv"), default=4))
+        self.scratch = torch.zeros(64 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
+        self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    # ---- GEMM routing ------------------------------------------------------
+    def _gemm(self, stream, m, n, k, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
+              bias=None, bias_sb=0, mask=None, mask_sm=0, mask_sn=0, mask_sb=0, act=0, pre=None):
+        nb = self.nrep
+        tc_ok = (self.use_tc and pre is None and a_sk == 1 and b_sk == 1 and a_sm % 4 == 0 and
+                 b_sn % 4 == 0 and a % 16 == 0 and bm % 16 == 0 and m >= 128 and
+                 (nb == 1 or (a_sb % 4 == 0 and b_sb % 4 == 0)) and m * n * k >= TC_MIN_FLOPS)
+        if tc_ok:
+            d = TcGemmDesc(m, n, k, nb, a, a_sm, a_sb, bm, b_sn, b_sb, c, c_sm, c_sn, c_sb,
+                           bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, act, 0, self.precision)
+            _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream), "tc_gemm")
+        else:
+            d = GemmDesc(m, n, k, nb, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
+                         bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0)
+            _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream), "gemm")
+
+    # ---- passes ----------------------------------------------------------------
+    def forward(self, W: torch.Tensor, stream: int, x: torch.Tensor | None = None) -> torch.Tensor:
+        """Forward of all replicas on self.x (or ``x``, same shape); returns
+        the logits tensor (nrep, b*classes pitch)."""
+        lib = _lib.load()
+        b, nb = self.b, self.nrep
+        wp, ldw = W.data_ptr(), W.stride(0)
+        xin = self.x if x is None else x
+        cur, cur_sb = xin.data_ptr(), xin.stride(0)
+        cur_d = nchw(b, self.c0, self.h0, self.w0)
+        cur_flat = True   # current tensor is (b, features) row-major
+        for i, L in enumerate(self.layers):
+            out = self.outs[i]
+            o, o_sb = out.data_ptr(), out.stride(0)
+            if L.kind == "conv":
+                col = self.cols[i]
+                lay = L.lay
+                _lib.check(lib.esgd_im2col_f32(col.data_ptr(), L.kp, col.stride(0), cur, cur_d, cur_sb,
+                                               lay.k, lay.k, lay.stride, lay.pad, L.hout, L.wout, nb,
+                                               stream), "im2col")
+                self._gemm(stream, b * L.hout * L.wout, L.cout, L.k,
+                           col.data_ptr(), L.kp, 1, col.stride(0),
+                           wp + 4 * L.w_off, 1, L.k, ldw,
+                           o, L.cout, 1, o_sb, bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act)
+                cur_d = nhwc(b, L.cout, L.hout, L.wout)
+                cur_flat = False
+            elif L.kind == "pool":
+                lay = L.lay
+                yd = nhwc(b, L.cout, L.hout, L.wout)
+                _lib.check(lib.esgd_maxpool_fwd_f32(o, yd, o_sb, self.amax[i].data_ptr(), cur, cur_d, cur_sb,
+                                                    lay.k, lay.stride, lay.pad, nb, stream), "maxpool")
+                cur_d = yd
+            else:
+                if L.flatten_in:
+                    f = self.flat[i]
+                    _lib.check(lib.esgd_copy4_f32(f.data_ptr(), nchw(b, L.cin, L.hin, L.win), f.stride(0),
+                                                  cur, cur_d, cur_sb, nb, stream), "flatten")
+                    cur, cur_sb = f.data_ptr(), f.stride(0)
+                fan_in = L.cin * L.hin * L.win
+                pre = self.pre[i]
+                self._gemm(stream, b, L.cout, fan_in, cur, fan_in, 1, cur_sb,
+                           wp + 4 * L.w_off, L.cout, 1, ldw, o, L.cout, 1, o_sb,
+                           bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act,
+                           pre=None if pre is None else pre.data_ptr())
+                cur_d = nchw(b, L.cout, 1, 1)
+                cur_flat = True
+            cur, cur_sb = o, o_sb
+        return self.outs[-1]
+
+    def _input_of(self, i: int):
+        """(ptr, batch stride, tensor4, producer-act) of layer i's input."""
+        b = self.b
+        if i == 0:
+            return (self.x.data_ptr(), self.x.stride(0), nchw(b, self.c0, self.h0, self.w0), 0)
+        P = self.layers[i - 1]
+        t = self.outs[i - 1]
+        d = nhwc(b, P.cout, P.hout, P.wout) if P.kind in ("conv", "pool") else nchw(b, P.cout, 1, 1)
+        act = P.act if P.kind != "pool" else 0
+        return (t.data_ptr(), t.stride(0), d, act)
+
+    def _other(self, t: torch.Tensor) -> torch.Tensor:
+        return self.d_b if t is self.d_a else self.d_a
+
+    def _act_bwd(self, d: torch.Tensor, z_ptr: int, z_sb: int, n_el: int, act: int, stream: int) -> None:
+        # d[r] *= act'(z[r]) for each replica (relu'(a) == relu'(z) for a = relu(z))
+        lib = _lib.load()
+        for r in range(self.nrep):
+            _lib.check(lib.esgd_act_bwd_f32(d.data_ptr() + 4 * r * d.stride(0), z_ptr + 4 * r * z_sb,
+                                            n_el, act, stream), "act_bwd")
+
+    def gradient(self, G: torch.Tensor, W: torch.Tensor, stream: int) -> None:
+        """G[r] = d(mean CE)/dW[r] on the sampled batch in self.x/self.y."""
+        lib = _lib.load()
+        b, nb = self.b, self.nrep
+        wp, ldw = W.data_ptr(), W.stride(0)
+        gp, ldg = G.data_ptr(), G.stride(0)
+        logits = self.forward(W, stream)
+        # dlogits = (softmax - onehot)/rows, in place over the logits (kernels.py:85-106)
+        _lib.check(lib.esgd_softmax_xent_f32(logits.data_ptr(), self.row_loss.data_ptr(), logits.data_ptr(),
+                                             self.classes, logits.stride(0), self.y.data_ptr(),
+                                             self.y.stride(0), b, self.classes, nb,
+                                             self.bad_label.data_ptr(), stream), "softmax_xent")
+        dcur = logits
+        first_param = next(j for j, L in enumerate(self.layers) if L.kind != "pool")
+        for i in range(len(self.layers) - 1, -1, -1):
+            L = self.layers[i]
+            d_sb = dcur.stride(0)
+            xin, x_sb, xd, pact = self._input_of(i)
+            need_dx = i > first_param
+            if L.kind == "dense":
+                fan_in = L.cin * L.hin * L.win
+                a_ptr, a_sb = (self.flat[i].data_ptr(), self.flat[i].stride(0)) if L.flatten_in else (xin, x_sb)
+                # dW[in, out] = x^T . delta   (network.py:194)
+                self._gemm(stream, fan_in, L.cout, b, a_ptr, 1, fan_in, a_sb,
+                           dcur.data_ptr(), L.cout, 1, d_sb,
+                           gp + 4 * L.w_off, L.cout, 1, ldg)
+                # db = sum_rows delta   (network.py:195)
+                _lib.check(lib.esgd_colsum_f32(gp + 4 * L.b_off, ldg, dcur.data_ptr(), L.cout, d_sb, b, L.cout,
+                                               nb, self.scratch.data_ptr(), stream), "colsum")
+                if not need_dx:
+                    continue
+                # delta_prev = (delta . W^T) * act'(z_prev)   (network.py:197-199)
+                dnext = self._other(dcur)
+                mask = xin if (pact == 1 and not L.flatten_in) else None
+                self._gemm(stream, b, fan_in, L.cout, dcur.data_ptr(), L.cout, 1, d_sb,
+                           wp + 4 * L.w_off, 1, L.cout, ldw,
+                           dnext.data_ptr(), fan_in, 1, dnext.stride(0),
+                           mask=mask, mask_sm=fan_in, mask_sn=1, mask_sb=x_sb)
+                if pact in (2, 3):
+                    self._act_bwd(dnext, self.pre[i - 1].data_ptr(), self.pre[i - 1].stride(0), b * fan_in,
+                                  pact, stream)
+                if L.flatten_in:
+                    # (c,h,w)-flat gradient back to the producer's NHWC layout
+                    dback = self._other(dnext)
+                    _lib.check(lib.esgd_copy4_f32(dback.data_ptr(), xd, dback.stride(0), dnext.data_ptr(),
+                                                  nchw(b, L.cin, L.hin, L.win), dnext.stride(0), nb, stream),
+                               "unflatten")
+                    if pact == 1:
+                        self._act_bwd(dback, xin, x_sb, b * fan_in, 1, stream)
+                    dnext = dback
+                dcur = dnext
+            elif L.kind == "pool":
+                lay = L.lay
+                yd = nhwc(b, L.cout, L.hout, L.wout)
+                dnext = self._other(dcur)
+                mask = xin if pact == 1 else None
+                _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd, d_sb,
+                                                    self.amax[i].data_ptr(), mask, lay.k, lay.stride, lay.pad,
+                                                    nb, stream), "maxpool_bwd")
+                dcur = dnext
+            else:  # conv
+                lay = L.lay
+                col = self.cols[i]
+                pix = b * L.hout * L.wout
+                # dW[Cout, K] = delta^T . col
+                self._gemm(stream, L.cout, L.k, pix, dcur.data_ptr(), 1, L.cout, d_sb,
+                           col.data_ptr(), L.kp, 1, col.stride(0),
+                           gp + 4 * L.w_off, L.k, 1, ldg)
+                _lib.check(lib.esgd_colsum_f32(gp + 4 * L.b_off, ldg, dcur.data_ptr(), L.cout, d_sb, pix, L.cout,
+                                               nb, self.scratch.data_ptr(), stream), "colsum")
+                if not need_dx:
+                    continue
+                # dcol[pix, K] = delta . W ; dx = col2im(dcol) (relu-masked by the producer)
+                self._gemm(stream, pix, L.k, L.cout, dcur.data_ptr(), L.cout, 1, d_sb,
+                           wp + 4 * L.w_off, L.k, 1, ldw,
+                           self.dcol.data_ptr(), L.kp, 1, self.dcol.stride(0))
+                dnext = self._other(dcur)
+                mask = xin if pact == 1 else None
+                _lib.check(lib.esgd_col2im_f32(dnext.data_ptr(), xd, dnext.stride(0), self.dcol.data_ptr(), L.kp,
+                                               self.dcol.stride(0), lay.k, lay.k, lay.stride, lay.pad,
+                                               L.hout, L.wout, mask, nb, stream), "col2im")
+                dcur = dnext

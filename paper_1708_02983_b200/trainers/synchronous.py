@@ -1,0 +1,231 @@
+"""Bulk-synchronous elastic averaging on the device — the north-star path
+(reference trainers/synchronous.py:47-219).
+
+Per round, exactly the reference's arithmetic (``_sync_round``, :57-64):
+every worker i computes g_i at W_i(t); S = sum_i W_i(t) (pre-update);
+W_i(t+1) = (W_i - eta g_i) - eta rho (W_i - C_t); C(t+1) = C_t + eta rho (S - P C_t).
+
+B200 mapping:
+* one process per GPU (torchrun); each process holds P/world worker replicas
+  as rows of one (nrep, ldw) fp32 tensor plus a replica of the center;
+* S = local fixed-order replica sum (the reference's binomial order, exact
+  when all workers are local) + one NCCL allreduce of the packed buffer over
+  NVLink/NVSwitch (replaces tree_sum / Alg. 3's broadcast+reduce);
+* the worker steps of all local replicas and the center step are one fused
+  HBM-streaming kernel (esgd_sync_update_f32), every rank updating its own
+  identical center replica;
+* ``sync-easgd3``: the sum+allreduce runs on a side stream concurrently with
+  the round's forward/backward (both only read W(t)); 1 and 2
+  serialize it. Placement differences between easgd1/2 are pricing-only in
+  the reference (:1-28) and arithmetic-identical here as there;
+* the round (sampling, forward/backward, sum, allreduce, update) is captured
+  once in a CUDA graph and replayed, so the host cost per round is one launch.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from ..device import require_cuda, round_up, stream_ptr
+from ..errors import InputError
+from ..fabric.collectives import allreduce_sum_, local_workers, replica_sum_, world
+from ..fabric.engine import CATEGORIES
+from ..rng import stream_seed
+from ..updates import sync_update_
+from .common import Recorder
+from .config import TrainerConfig
+from .records import RunRecord
+
+SYNC_METHODS = ("sync-easgd1", "sync-easgd2", "sync-easgd3", "group-easgd")
+
+
+class SyncEngine:
+    """Device state and one-round step of a Sync-EASGD run on this rank."""
+
+    def __init__(self, cfg: TrainerConfig, problem, use_graph: bool = True, use_tc: bool = True,
+                 profile_rounds: int = 2):
+        if cfg.method not in SYNC_METHODS:
+            raise InputError(f"not a bulk-synchronous method: {cfg.method}")
+        self.cfg, self.problem = cfg, problem
+        self.P = cfg.cluster.workers
+        self.world, self.rank = world()
+        mine = local_workers(self.P, self.world, self.rank)
+        self.nrep = len(mine)
+        self.first = mine.start
+        self.groups = cfg.cluster.groups if cfg.method == "group-easgd" else 1
+        if self.groups > 1 and self.world > 1 and (self.nrep % (self.P // self.groups)) and \
+                ((self.P // self.groups) % self.nrep):
+            raise InputError("group-easgd across processes needs groups aligned to ranks")
+        self.device = require_cuda()
+        self.overlap = cfg.method == "sync-easgd3"
+        init = np.asarray(problem.init_weights(), dtype=np.float32).reshape(-1)
+        self.n = n = init.size
+        self.ldw = ld = round_up(n, 64)
+        dev = self.device
+        self.W = torch.zeros((self.nrep, ld), dtype=torch.float32, device=dev)
+        self.W[:, :n] = torch.from_numpy(init).to(dev)
+        self.G = torch.zeros_like(self.W)
+        self.C = torch.zeros(ld, dtype=torch.float32, device=dev)
+        self.C[:n] = self.W[0, :n]
+        self.S = torch.zeros(ld, dtype=torch.float32, device=dev)
+        gsize = self.P // self.groups
+        self.local_groups = max(1, self.nrep // gsize) if self.groups > 1 else 1
+        self.partials = (torch.zeros((self.local_groups, ld), dtype=torch.float32, device=dev)
+                         if self.local_groups > 1 else None)
+        self.plan = problem.bind(dev, self.nrep, cfg.batch_size, ld, use_tc=use_tc)
+        self.plan.set_streams([stream_seed(cfg.seed, w) for w in range(self.first, self.first + self.nrep)])
+        self.comm = torch.cuda.Stream(device=dev)
+        self.use_graph = use_graph
+        self.graph = None
+        self.profile_rounds = profile_rounds
+        self.phase_ms = {c: 0.0 for c in CATEGORIES}
+        self.profiled = 0
+        if self.world > 1:  # bring NCCL up outside any capture
+            allreduce_sum_(torch.zeros(1, device=dev))
+            torch.cuda.synchronize()
+
+    # ---- one round ------------------------------------------------------------
+    def _sum(self, stream) -> None:
+        s = stream_ptr(stream)
+        if self.partials is not None:
+            gsize = self.nrep // self.local_groups
+            for g in range(self.local_groups):
+                replica_sum_(self.partials[g], self.W[g * gsize:(g + 1) * gsize], self.n, stream)
+            replica_sum_(self.S, self.partials, self.n, stream)
+        else:
+            replica_sum_(self.S, self.W, self.n, stream)
+        allreduce_sum_(self.S)
+
+    def _gradient(self, stream) -> None:
+        self.plan.gradient(self.G, self.W, stream_ptr(stream))
+
+    def _update(self, stream) -> None:
+        sync_update_(self.W, self.G, self.C, self.S, self.n, self.P, self.cfg.hyper, stream)
+
+    def step_eager(self, ev: dict | None = None) -> None:
+        cs = torch.cuda.current_stream()
+        rec = (lambda k, s: ev[k].record(s)) if ev is not None else (lambda k, s: None)
+        rec("t0", cs)
+        if self.overlap:
+            self.comm.wait_stream(cs)
+            with torch.cuda.stream(self.comm):
+                rec("c0", self.comm)
+                self._sum(self.comm)
+                rec("c1", self.comm)
+            self._gradient(cs)
+            rec("g1", cs)
+            cs.wait_stream(self.comm)
+        else:
+            self._gradient(cs)
+            rec("g1", cs)
+            rec("c0", cs)
+            self._sum(cs)
+            rec("c1", cs)
+        rec("j", cs)
+        self._update(cs)
+        rec("u1", cs)
+
+    def _capture(self) -> None:
+        g = torch.cuda.CUDAGraph()
+        # capture on a side stream (torch requirement); the graph then replays anywhere
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        rng_before = self.plan.rng.state.clone() if hasattr(self.plan, "rng") else None
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.step_eager()
+        torch.cuda.current_stream().wait_stream(s)
+        if rng_before is not None:  # capture does not execute, but keep state untouched
+            self.plan.rng.state.copy_(rng_before)
+        self.graph = g
+
+    def step(self) -> None:
+        """Enqueue one round (graph replay once captured)."""
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        if self.use_graph and self.profiled >= self.profile_rounds:
+            try:
+                self._capture()
+            except Exception:  # capture unsupported here (e.g. NCCL): stay eager
+                self.use_graph = False
+                torch.cuda.synchronize()
+            if self.graph is not None:
+                self.graph.replay()
+                return
+        if self.profiled < self.profile_rounds:
+            self._profiled_step()
+        else:
+            self.step_eager()
+
+    def _profiled_step(self) -> None:
+        names = ("t0", "c0", "c1", "g1", "j", "u1")
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in names}
+        self.step_eager(ev)
+        ev["u1"].synchronize()
+        fb = ev["t0"].elapsed_time(ev["g1"])
+        if self.overlap:
+            exposed = max(0.0, ev["g1"].elapsed_time(ev["j"]))
+        else:
+            exposed = ev["c0"].elapsed_time(ev["c1"])
+        self.phase_ms["forward_backward"] += fb
+        self.phase_ms["peer_param"] += exposed
+        self.phase_ms["worker_update"] += ev["j"].elapsed_time(ev["u1"])
+        self.profiled += 1
+
+    # ---- results --------------------------------------------------------------
+    def center_host(self) -> np.ndarray:
+        return self.C[:self.n].cpu().numpy()
+
+    def workers_host(self) -> list[np.ndarray]:
+        local = self.W[:, :self.n].contiguous()
+        if self.world > 1:
+            bufs = [torch.empty_like(local) for _ in range(self.world)]
+            dist.all_gather(bufs, local)
+            local = torch.cat(bufs)
+        return [local[i].cpu().numpy() for i in range(self.P)]
+
+    def breakdown(self, total_s: float) -> dict[str, float]:
+        out = {c: 0.0 for c in CATEGORIES}
+        if self.profiled:
+            per_round = {k: v / self.profiled / 1e3 for k, v in self.phase_ms.items()}
+            tot = sum(per_round.values())
+            scale = total_s / (tot * self.cfg.iterations) if tot > 0 else 0.0
+            for k, v in per_round.items():
+                out[k] = v * self.cfg.iterations * scale
+        return out
+
+
+def _max_over_ranks(x: float, device) -> float:
+    if world()[0] > 1:
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def run_synchronous(cfg: TrainerConfig, problem, cm=None, **engine_kw) -> RunRecord:
+    eng = SyncEngine(cfg, problem, **engine_kw)
+    rec = Recorder(problem, cfg.eval_every, cfg.iterations)
+    elapsed = 0.0
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record()
+    for t in range(cfg.iterations):
+        eng.step()
+        if rec.due(t + 1):
+            t1.record()
+            t1.synchronize()
+            elapsed += t0.elapsed_time(t1) / 1e3
+            rec.record(t + 1, _max_over_ranks(elapsed, eng.device), eng.C[:eng.n])
+            t0.record()
+    total = _max_over_ranks(elapsed, eng.device)
+    info = {"engine": "cuda", "world": eng.world, "replicas_per_rank": eng.nrep,
+            "graph": eng.graph is not None, "overlap": eng.overlap}
+    return rec.build(cfg.method, total, eng.center_host(), breakdown=eng.breakdown(total),
+                     worker_weights=eng.workers_host(), engine_info=info)

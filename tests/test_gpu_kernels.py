@@ -1,0 +1,224 @@
+"""Kernel-level parity on the B200: libesgd vs the reference's own outputs
+(golden fixtures) and the pinned oracle. Update rules, the tree sum and the
+sampled indices are bitwise; GEMMs are checked against float64."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import esgd_oracle as O
+from paper_1708_02983_b200 import _lib, updates as U
+from paper_1708_02983_b200.fabric import collectives, engine
+from paper_1708_02983_b200.device import stream_ptr
+from _gpu_util import dev, host, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def test_library_on_b200():
+    lib = _lib.load()
+    assert lib.esgd_device_ok(0) == 1, _lib.last_error()
+
+
+def test_update_rules_bitwise_vs_reference(golden):
+    g = golden("updates")
+    eta, rho, mu, P = (float(x) for x in g["scalars"])
+    w, v, gr, c, s = (dev(a) for a in g["float32_in"])
+    assert np.array_equal(host(U.easgd_worker_step(w, gr, c, eta, rho)), g["float32_worker"])
+    assert np.array_equal(host(U.easgd_center_step_from_sum(c, s, int(P), eta, rho)),
+                          g["float32_center_from_sum"])
+    assert np.array_equal(host(U.easgd_center_incremental(c, w, eta, rho)), g["float32_center_incr"])
+    mw, mv = U.measgd_worker_step(w, v, gr, c, eta, mu, rho)
+    assert np.array_equal(host(mw), g["float32_measgd_w"])
+    assert np.array_equal(host(mv), g["float32_measgd_v"])
+    assert np.array_equal(host(U.sgd_step(w, gr, eta)), g["float32_sgd"])
+    a, b = U.msgd_step(w, v, gr, eta, mu)
+    assert np.array_equal(host(a), g["float32_msgd_w"]) and np.array_equal(host(b), g["float32_msgd_v"])
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 13])
+def test_tree_sum_bitwise_vs_reference(golden, p):
+    g = golden("updates")
+    bufs = [dev(x) for x in g[f"float32_tree_in_{p}"]]
+    assert np.array_equal(host(collectives.tree_sum(bufs)), g[f"float32_tree_out_{p}"])
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 1029, 65536 + 7])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_fused_sync_update_bitwise(n, offset):
+    """fused worker+center kernel == reference op sequence, incl. unaligned
+    (offset) and tail sizes, for 1..3 local replicas."""
+    rng = np.random.default_rng(n + offset)
+    for nrep in (1, 3):
+        ld = n + 64 + offset
+        W0 = rng.standard_normal((nrep, ld)).astype(np.float32)
+        G0 = rng.standard_normal((nrep, ld)).astype(np.float32)
+        C0 = rng.standard_normal(ld).astype(np.float32)
+        S0 = rng.standard_normal(ld).astype(np.float32)
+        hy = U.HyperParams(eta=0.05, rho=0.25)
+        W, G, Cc, S = dev(W0), dev(G0), dev(C0), dev(S0)
+        Wv, Gv = W[:, offset:], G[:, offset:]
+        _lib.call("esgd_sync_update_f32", Wv.data_ptr(), ld, Gv.data_ptr(), ld, nrep,
+                  Cc[offset:].data_ptr(), S[offset:].data_ptr(), n, hy.eta32, hy.etarho32, 4, stream_ptr())
+        ew = [O.easgd_worker_step(W0[r, offset:offset + n], G0[r, offset:offset + n],
+                                  C0[offset:offset + n], 0.05, 0.25) for r in range(nrep)]
+        ec = O.easgd_center_step_from_sum(C0[offset:offset + n], S0[offset:offset + n], 4, 0.05, 0.25)
+        for r in range(nrep):
+            assert np.array_equal(host(W)[r, offset:offset + n], ew[r])
+            assert np.array_equal(host(W)[r, offset + n:], W0[r, offset + n:])  # untouched
+        assert np.array_equal(host(Cc)[offset:offset + n], ec)
+
+
+def test_hogwild_single_stream_exact():
+    rng = np.random.default_rng(1)
+    n = 4099
+    c0, w0, s0 = (rng.standard_normal(n).astype(np.float32) for _ in range(3))
+    c = dev(c0)
+    engine.hogwild_elastic_apply(c, dev(w0), dev(s0), float(np.float32(0.05 * 0.25)))
+    expect = c0.copy()
+    O.hogwild_apply(expect, (0.05 * 0.25) * (w0 - s0))
+    assert np.array_equal(host(c), expect)
+
+
+def test_hogwild_concurrent_streams_commutative():
+    """many streams racing on one center: the sum of integer-valued deltas is
+    exact regardless of interleaving (fabric/engine.py:156-166 contract)."""
+    n = 1 << 20
+    c = torch.zeros(n, device="cuda")
+    deltas = [torch.full((n,), float(k + 1), device="cuda") for k in range(16)]
+    streams = [torch.cuda.Stream() for _ in range(16)]
+    torch.cuda.synchronize()
+    for k, s in enumerate(streams):
+        with torch.cuda.stream(s):
+            engine.hogwild_apply(c, deltas[k])
+    torch.cuda.synchronize()
+    assert torch.all(c == float(sum(range(1, 17))))
+
+
+def test_sampled_indices_bitwise_vs_reference(golden):
+    g = golden("rng")
+    seed = O.stream_seed(3, 2)
+    out = torch.empty(256, dtype=torch.int64, device="cuda")
+    _lib.call("esgd_randint_u64", out.data_ptr(), seed, 0, 256, 60000, stream_ptr())
+    assert np.array_equal(host(out), g["randint_60000"])
+
+
+def test_sample_batch_gathers_and_advances_counter():
+    rng = np.random.default_rng(0)
+    n, d, b, nrep = 1000, 36, 17, 3
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Y = rng.integers(0, 10, n).astype(np.int32)
+    seeds = [O.stream_seed(9, w) for w in range(nrep)]
+    state = torch.tensor(np.array([[s, 5] for s in seeds], dtype=np.uint64).view(np.int64), device="cuda")
+    ticket = torch.zeros(nrep, dtype=torch.int32, device="cuda")
+    xo = torch.zeros((nrep, b * d), device="cuda")
+    yo = torch.zeros((nrep, b), dtype=torch.int32, device="cuda")
+    for rnd in range(2):
+        _lib.call("esgd_sample_batch_f32", xo.data_ptr(), xo.stride(0), yo.data_ptr(), None,
+                  dev(X).data_ptr(), dev(Y, torch.int32).data_ptr(), n, d, state.data_ptr(),
+                  ticket.data_ptr(), b, nrep, stream_ptr())
+        torch.cuda.synchronize()
+        for r in range(nrep):
+            o = O.CounterRng(seeds[r], 5 + rnd * b)
+            xs, ys = O.sample_batch(X, Y, b, o)
+            assert np.array_equal(host(xo[r]).reshape(b, d), xs)
+            assert np.array_equal(host(yo[r]), ys)
+    assert np.all(host(state)[:, 1] == 5 + 2 * b)
+
+
+def test_softmax_xent_vs_reference(golden):
+    g = golden("net")
+    logits = g["xent_logits"].astype(np.float32)
+    labels = g["xent_labels"].astype(np.int32)
+    rows, cols = logits.shape
+    lg = dev(logits)
+    dl = torch.empty_like(lg)
+    rl = torch.empty(rows, device="cuda")
+    _lib.call("esgd_softmax_xent_f32", dl.data_ptr(), rl.data_ptr(), lg.data_ptr(), cols, rows * cols,
+              dev(labels, torch.int32).data_ptr(), rows, rows, cols, 1, None, stream_ptr())
+    assert rel_err(host(dl), g["xent_dlogits"]) < 1e-6
+    assert abs(float(host(rl).astype(np.float64).mean()) - g["xent_loss"][0]) < 1e-6
+
+
+def _gemm_ref(A, B):
+    return A.astype(np.float64) @ B.astype(np.float64)
+
+
+@pytest.mark.parametrize("m,n,k,batch", [(1, 1, 1, 1), (64, 10, 500, 2), (130, 70, 33, 3), (257, 500, 800, 1)])
+def test_ffma_gemm_strided(m, n, k, batch):
+    rng = np.random.default_rng(m * n + k)
+    A = rng.standard_normal((batch, m, k)).astype(np.float32)
+    B = rng.standard_normal((batch, n, k)).astype(np.float32)  # stored N x K -> B(k,n) stride (1, k)
+    bias = rng.standard_normal((batch, n)).astype(np.float32)
+    Ad, Bd, bd = dev(A), dev(B), dev(bias)
+    Cd = torch.zeros((batch, m, n), device="cuda")
+    d = _lib.GemmDesc(m, n, k, batch, Ad.data_ptr(), k, 1, m * k, Bd.data_ptr(), 1, k, n * k,
+                      Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, None, 1, 0)
+    _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream_ptr()))
+    for z in range(batch):
+        ref = np.maximum(_gemm_ref(A[z], B[z].T) + bias[z], 0)
+        assert rel_err(host(Cd[z]), ref) < 1e-6
+
+
+@pytest.mark.parametrize("m,n,k,batch", [(128, 64, 32, 1), (300, 50, 500, 2), (1024, 192, 1600, 1),
+                                         (4096, 128, 363, 1), (257, 1000, 4096, 1), (129, 20, 25, 3)])
+@pytest.mark.parametrize("precision,tol", [(3, 2e-6), (1, 5e-3)])
+def test_tcgen05_gemm(m, n, k, batch, precision, tol):
+    """tcgen05 kind::tf32 GEMM: 3xTF32 reaches fp32-grade error; plain TF32 ~1e-3."""
+    rng = np.random.default_rng(m + n + k)
+    kp = (k + 3) // 4 * 4
+    A = np.zeros((batch, m, kp), np.float32)
+    B = np.zeros((batch, n, kp), np.float32)
+    A[:, :, :k] = rng.standard_normal((batch, m, k))
+    B[:, :, :k] = rng.standard_normal((batch, n, k))
+    bias = rng.standard_normal((batch, n)).astype(np.float32)
+    Ad, Bd, bd = dev(A), dev(B), dev(bias)
+    Cd = torch.zeros((batch, m, n), device="cuda")
+    d = _lib.TcGemmDesc(m, n, k, batch, Ad.data_ptr(), kp, m * kp, Bd.data_ptr(), kp, n * kp,
+                        Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, 0, 0, precision)
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    torch.cuda.synchronize()
+    for z in range(batch):
+        ref = _gemm_ref(A[z, :, :k], B[z, :, :k].T) + bias[z]
+        assert rel_err(host(Cd[z]), ref) < tol, (z, rel_err(host(Cd[z]), ref))
+
+
+def test_im2col_col2im_adjoint_and_oracle():
+    rng = np.random.default_rng(3)
+    n, c, h, w, k, s, p = 2, 3, 13, 11, 5, 2, 2
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    K = c * k * k
+    kp = (K + 3) // 4 * 4
+    col = torch.zeros((n * oh * ow, kp), device="cuda")
+    _lib.call("esgd_im2col_f32", col.data_ptr(), kp, 0, dev(x).data_ptr(), _lib.nchw(n, c, h, w), 0,
+              k, k, s, p, oh, ow, 1, stream_ptr())
+    ref, _, _ = O._im2col(x, k, s, p)
+    assert np.array_equal(host(col)[:, :K], ref)
+    dcol = rng.standard_normal((n * oh * ow, kp)).astype(np.float32)
+    dx = torch.zeros((n, c, h, w), device="cuda")
+    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dev(dcol).data_ptr(), kp, 0,
+              k, k, s, p, oh, ow, None, 1, stream_ptr())
+    exp = O._col2im(dcol[:, :K].copy(), (n, c, h, w), k, s, p, oh, ow)
+    assert np.array_equal(host(dx), exp)
+
+
+def test_maxpool_fwd_bwd_vs_oracle():
+    rng = np.random.default_rng(4)
+    n, c, h, w, k, s, p = 2, 4, 15, 15, 3, 2, 1
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    x[0, 0, :4, :4] = 1.0  # ties: first max in scan order wins
+    y = torch.zeros((n, c, oh, ow), device="cuda")
+    am = torch.zeros((n, c, oh, ow), dtype=torch.int32, device="cuda")
+    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), dev(x).data_ptr(),
+              _lib.nchw(n, c, h, w), 0, k, s, p, 1, stream_ptr())
+    ey, ea = O._maxpool(x, k, s, p)
+    assert np.array_equal(host(y), ey) and np.array_equal(host(am), ea)
+    dy = rng.standard_normal((n, c, oh, ow)).astype(np.float32)
+    dx = torch.zeros((n, c, h, w), device="cuda")
+    _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dev(dy).data_ptr(),
+              _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), None, k, s, p, 1, stream_ptr())
+    assert np.array_equal(host(dx), O._maxpool_bwd(dy, ea, (n, c, h, w)))
