@@ -73,6 +73,12 @@ int esgd_measgd_update_f32(float* w, float* v, const float* g, const float* c, i
 int esgd_center_incr_f32(float* c_out, const float* c, const float* w, int64_t n,
                          float etarho, esgd_stream_t stream);
 
+/* original EASGD round (trainers/roundrobin.py:120-124), fused, in place:
+ * from the same old (w, c):  w = (w - eta*g) - etarho*(w - c);
+ *                            c = c + etarho*(w_old - c).   20 B/param.      */
+int esgd_exchange_update_f32(float* w, const float* g, float* c, int64_t n, float eta,
+                             float etarho, esgd_stream_t stream);
+
 /* sgd_step / msgd_step, updates.py:71-82 (in place) */
 int esgd_sgd_step_f32(float* w, const float* g, int64_t n, float eta, esgd_stream_t stream);
 int esgd_msgd_step_f32(float* w, float* v, const float* g, int64_t n, float eta, float mu,
@@ -121,6 +127,10 @@ int esgd_quadratic_grad_f32(float* G, int64_t ldg, const float* W, int64_t ldw, 
  * element strides (row/col/batch) for every operand; optional epilogue mask
  * multiplies by (mask > 0) (relu-grad), optional c_pre keeps the
  * pre-activation; accumulate adds into C. fp32 FFMA, for the small GEMMs.
+ * When the output has few tiles and k is long (weight gradients reduce over
+ * every pixel of the batch) the reduction is split across CTAs into `ws`
+ * (ws_floats floats of device scratch, may be NULL) and combined in a fixed
+ * order, so results stay deterministic.
  * (network.py:166-171 forward, :194-199 backward, kernels.py:22-26)        */
 typedef struct {
   int32_t m, n, k, batch;
@@ -132,6 +142,8 @@ typedef struct {
   float* c_pre;
   int32_t act;
   int32_t accumulate;
+  float* ws;
+  int64_t ws_floats;
 } esgd_gemm_desc;
 int esgd_gemm_f32(const esgd_gemm_desc* desc, esgd_stream_t stream);
 
@@ -175,7 +187,7 @@ int esgd_argmax_rows_f32(int32_t* out, const float* x, int64_t ld, int32_t rows,
 
 /* column sums over rows: out[z*out_sb + j] = sum_i x[z][i*ld + j] (bias grad,
  * network.py:195). Deterministic fixed-order two-pass reduction.
- * scratch: >= 64*cols*batch floats.                                         */
+ * scratch: >= 256*cols*batch floats.                                         */
 int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld, int64_t x_sb,
                     int64_t rows, int32_t cols, int32_t batch, float* scratch,
                     esgd_stream_t stream);

@@ -31,6 +31,7 @@ class GemmDesc(C.Structure):
         ("mask", vp), ("mask_sm", i64), ("mask_sn", i64), ("mask_sb", i64),
         ("c_pre", vp),
         ("act", i32), ("accumulate", i32),
+        ("ws", vp), ("ws_floats", i64),
     ]
 
 
@@ -68,6 +69,7 @@ _SIGS = {
     "esgd_sync_update_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, f32, f32, i32, vp]),
     "esgd_measgd_update_f32": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, f32, vp]),
     "esgd_center_incr_f32": (C.c_int, [vp, vp, vp, i64, f32, vp]),
+    "esgd_exchange_update_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
     "esgd_sgd_step_f32": (C.c_int, [vp, vp, i64, f32, vp]),
     "esgd_msgd_step_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
     "esgd_hogwild_apply_f32": (C.c_int, [vp, vp, vp, i64, f32, vp]),

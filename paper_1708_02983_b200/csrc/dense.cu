@@ -38,10 +38,27 @@ __device__ __forceinline__ float act_grad_mul(float d, float z, int act) {
 // through shared memory (A transposed so the inner loop reads float4 rows).
 constexpr int BM = 64, BN = 64, BK = 16;
 
-__global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
+__device__ __forceinline__ float epilogue(const esgd_gemm_desc& d, float acc, int z, int gm, int gn,
+                                          float* C, float* Cp, int64_t off) {
+  const float* bias = d.bias ? d.bias + z * d.bias_sb : nullptr;
+  const float* mask = d.mask ? d.mask + z * d.mask_sb : nullptr;
+  float v = acc;
+  if (d.accumulate) v = __fadd_rn(C[off], v);
+  if (bias) v = __fadd_rn(v, bias[gn]);
+  if (Cp) Cp[off] = v;
+  v = act_apply(v, d.act);
+  if (mask) v = __fmul_rn(v, mask[(int64_t)gm * d.mask_sm + (int64_t)gn * d.mask_sn] > 0.f ? 1.f : 0.f);
+  return v;
+}
+
+// splits > 1: blockIdx.z = batch * splits + slice; each slice reduces its own
+// k range and writes raw partials to ws[z][slice][m][n]; k_gemm_reduce
+// combines slices in order and applies the epilogue.
+__global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d, int splits, int kchunk) {
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN + 4];
-  const int z = blockIdx.z;
+  const int z = blockIdx.z / splits, slice = blockIdx.z % splits;
+  const int kbeg = slice * kchunk, kend = min(d.k, kbeg + kchunk);
   const float* A = d.a + z * d.a_sb;
   const float* B = d.b + z * d.b_sb;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -63,11 +80,11 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
       int mm, kk;
       if (a_kfast) { mm = e >> 4; kk = e & 15; } else { mm = e & 63; kk = e >> 6; }
       int gm = m0 + mm, gk = k0 + kk;
-      ra[j] = (gm < d.m && gk < d.k) ? __ldg(A + (int64_t)gm * d.a_sm + (int64_t)gk * d.a_sk) : 0.f;
+      ra[j] = (gm < d.m && gk < kend) ? __ldg(A + (int64_t)gm * d.a_sm + (int64_t)gk * d.a_sk) : 0.f;
       int nn, kb;
       if (b_nfast) { nn = e & 63; kb = e >> 6; } else { nn = e >> 4; kb = e & 15; }
       int gn = n0 + nn, gkb = k0 + kb;
-      rb[j] = (gn < d.n && gkb < d.k) ? __ldg(B + (int64_t)gkb * d.b_sk + (int64_t)gn * d.b_sn) : 0.f;
+      rb[j] = (gn < d.n && gkb < kend) ? __ldg(B + (int64_t)gkb * d.b_sk + (int64_t)gn * d.b_sn) : 0.f;
     }
   };
   auto store_smem = [&](int buf) {
@@ -83,13 +100,13 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
     }
   };
 
-  const int nk = (d.k + BK - 1) / BK;
-  load_regs(0);
+  const int nk = (kend - kbeg + BK - 1) / BK;
+  load_regs(kbeg);
   store_smem(0);
   __syncthreads();
   for (int t = 0; t < nk; ++t) {
     const int buf = t & 1;
-    if (t + 1 < nk) load_regs((t + 1) * BK);  // prefetch next slab into registers
+    if (t + 1 < nk) load_regs(kbeg + (t + 1) * BK);  // prefetch next slab into registers
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       float4 a4 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
@@ -104,10 +121,22 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
     __syncthreads();
   }
 
+  if (splits > 1) {
+    float* P = d.ws + ((int64_t)z * splits + slice) * d.m * d.n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int gm = m0 + ty * 4 + i;
+      if (gm >= d.m) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int gn = n0 + tx * 4 + j;
+        if (gn < d.n) P[(int64_t)gm * d.n + gn] = acc[i][j];
+      }
+    }
+    return;
+  }
   float* C = d.c + z * d.c_sb;
   float* Cp = d.c_pre ? d.c_pre + z * d.c_sb : nullptr;
-  const float* bias = d.bias ? d.bias + z * d.bias_sb : nullptr;
-  const float* mask = d.mask ? d.mask + z * d.mask_sb : nullptr;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int gm = m0 + ty * 4 + i;
@@ -117,14 +146,28 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d) {
       int gn = n0 + tx * 4 + j;
       if (gn >= d.n) continue;
       int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
-      float v = acc[i][j];
-      if (d.accumulate) v = __fadd_rn(C[off], v);
-      if (bias) v = __fadd_rn(v, bias[gn]);
-      if (Cp) Cp[off] = v;
-      v = act_apply(v, d.act);
-      if (mask) v = __fmul_rn(v, mask[(int64_t)gm * d.mask_sm + (int64_t)gn * d.mask_sn] > 0.f ? 1.f : 0.f);
-      C[off] = v;
+      C[off] = epilogue(d, acc[i][j], z, gm, gn, C, Cp, off);
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gemm_reduce(esgd_gemm_desc d, int splits) {
+  const int64_t mn = (int64_t)d.m * d.n;
+  const int z = blockIdx.y;
+  float* C = d.c + z * d.c_sb;
+  float* Cp = d.c_pre ? d.c_pre + z * d.c_sb : nullptr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+    const float* P = d.ws + (int64_t)z * splits * mn + e;
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+    int s = 0;
+    for (; s + 3 < splits; s += 4) {  // four loads in flight per thread, fixed combine order
+      v0 += P[s * mn]; v1 += P[(s + 1) * mn]; v2 += P[(s + 2) * mn]; v3 += P[(s + 3) * mn];
+    }
+    for (; s < splits; ++s) v0 += P[s * mn];
+    const float v = (v0 + v1) + (v2 + v3);
+    const int gm = (int)(e / d.n), gn = (int)(e % d.n);
+    const int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
+    C[off] = epilogue(d, v, z, gm, gn, C, Cp, off);
   }
 }
 
@@ -204,9 +247,11 @@ __global__ void __launch_bounds__(128) k_argmax(int32_t* out, const float* x, in
   if (lane == 0) out[row] = bi == 0x7fffffff ? 0 : bi;
 }
 
-// Column sums, pass 1: CTA (32 cols x 8 row-lanes) over one row chunk,
-// fixed-order in-CTA combine, one partial per (chunk, col).
-__global__ void __launch_bounds__(256) k_colsum_partial(float* part, const float* x, int64_t ld,
+// Column sums, pass 1: CTA = 32 columns x 8 row-lanes over one row chunk;
+// every thread keeps 4 independent partial sums (loads in flight instead of a
+// serial dependency chain), combined in a fixed order, one partial per
+// (chunk, col).
+__global__ void __launch_bounds__(256) k_colsum_partial(float* part, const float* __restrict__ x, int64_t ld,
                                                         int64_t x_sb, int64_t rows, int cols,
                                                         int64_t chunk, float* out, int64_t out_sb,
                                                         int direct) {
@@ -214,10 +259,18 @@ __global__ void __launch_bounds__(256) k_colsum_partial(float* part, const float
   const int z = blockIdx.z, c = blockIdx.x * 32 + threadIdx.x, ty = threadIdx.y;
   const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
   const float* xz = x + z * x_sb;
-  float s = 0.f;
-  if (c < cols)
-    for (int64_t r = r0 + ty; r < r1; r += 8) s += xz[r * ld + c];
-  red[ty][threadIdx.x] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (c < cols) {
+    int64_t r = r0 + ty;
+    for (; r + 24 < r1; r += 32) {
+      s0 += __ldg(xz + r * ld + c);
+      s1 += __ldg(xz + (r + 8) * ld + c);
+      s2 += __ldg(xz + (r + 16) * ld + c);
+      s3 += __ldg(xz + (r + 24) * ld + c);
+    }
+    for (; r < r1; r += 8) s0 += __ldg(xz + r * ld + c);
+  }
+  red[ty][threadIdx.x] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (ty == 0 && c < cols) {
     float t = red[0][threadIdx.x];
@@ -232,9 +285,12 @@ __global__ void k_colsum_final(float* out, int64_t out_sb, const float* part, in
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cols * batch) return;
   int z = i / cols, c = i % cols;
-  float t = 0.f;
-  for (int k = 0; k < nchunk; ++k) t += part[((int64_t)z * nchunk + k) * cols + c];
-  out[z * out_sb + c] = t;
+  const float* p = part + (int64_t)z * nchunk * cols + c;
+  float t0 = 0.f, t1 = 0.f;
+  int k = 0;
+  for (; k + 1 < nchunk; k += 2) { t0 += p[(int64_t)k * cols]; t1 += p[(int64_t)(k + 1) * cols]; }
+  if (k < nchunk) t0 += p[(int64_t)k * cols];
+  out[z * out_sb + c] = t0 + t1;
 }
 
 }  // namespace
@@ -251,9 +307,26 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
   if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
   ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
   ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
-  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch);
+  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
+  int splits = 1;
+  if (d->ws && tiles < 2 * kNumSMs && d->k >= 4 * BK * 4) {
+    // enough slices to give ~2 CTAs per SM, each slice at least 4 slabs deep
+    int want = (2 * kNumSMs + tiles - 1) / tiles;
+    int maxs = d->k / (4 * BK);
+    splits = want < maxs ? want : maxs;
+    if (splits > 64) splits = 64;
+    while (splits > 1 && (int64_t)splits * d->m * d->n * d->batch > d->ws_floats) --splits;
+    if ((int64_t)d->batch * splits > 65535) splits = 1;
+  }
+  const int kchunk = ((d->k + splits - 1) / splits + BK - 1) / BK * BK;
+  if (splits > 1) splits = (d->k + kchunk - 1) / kchunk;
+  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch * splits);
   ESGD_REQUIRE(grid.y <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: m too large for the FFMA path");
-  k_gemm<<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d);
+  k_gemm<<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
+  if (splits > 1) {
+    dim3 rgrid(stride_grid((int64_t)d->m * d->n, 256, 4), d->batch);
+    k_gemm_reduce<<<rgrid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits);
+  }
   return check_launch("esgd_gemm_f32");
 }
 
@@ -300,8 +373,13 @@ extern "C" int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64
   ESGD_REQUIRE(rows >= 1 && cols >= 1 && batch >= 1 && ld >= cols, ESGD_ERR_SHAPE,
                "colsum: bad shape");
   ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "colsum: null buffer");
-  int64_t nchunk = (rows + 511) / 512;
-  if (nchunk > 64) nchunk = 64;
+  // ~2 CTAs per SM over the whole reduction, chunks of >= 128 rows
+  int64_t col_groups = (cols + 31) / 32;
+  int64_t nchunk = (rows + 127) / 128;
+  int64_t cap = (2 * kNumSMs + col_groups * batch - 1) / (col_groups * batch);
+  if (nchunk > cap) nchunk = cap;
+  if (nchunk > 256) nchunk = 256;
+  if (nchunk < 1) nchunk = 1;
   int64_t chunk = (rows + nchunk - 1) / nchunk;
   nchunk = (rows + chunk - 1) / chunk;
   ESGD_REQUIRE(nchunk == 1 || scratch, ESGD_ERR_INPUT, "colsum: scratch required for %lld rows",

@@ -9,11 +9,15 @@
 //   warps 2..5  : split warps — for 3xTF32 they rewrite each landed tile as
 //                 hi = x & 0xffffe000 (exact tf32) in place and lo = x - hi
 //                 into a twin buffer of identical (swizzled) layout, then
-//                 fence.proxy.async and arrive; afterwards they are the
-//                 epilogue (tcgen05.ld TMEM -> registers -> bias/act/mask).
+//                 fence.proxy.async and arrive.
 //   warp 1      : TMEM allocation and the single-thread tcgen05.mma issuer,
-//                 kind::tf32, M=128, N=BN, K=8 per instruction, accumulator
-//                 in TMEM; tcgen05.commit frees smem slots / signals epilogue.
+//                 kind::tf32, M=128, N=BN, K=8 per instruction, into one of
+//                 two TMEM accumulators per 128-wide K chunk; tcgen05.commit
+//                 frees smem slots and hands finished chunks to the drain.
+//   warps 6..9  : drain/epilogue — tcgen05.ld each chunk's partial sums and
+//                 add them into fp32 registers with RN adds (the tensor-core
+//                 accumulator alone loses ~1e-8*K relative), then bias/act/
+//                 mask and the store.
 //
 // 3xTF32: a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b, accumulated in fp32 in
 // TMEM — fp32-grade products (relative error ~2^-21), which the parity gate
@@ -29,7 +33,8 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;                  // 32 fp32 = 128 B = one swizzle atom row
-constexpr int kThreads = 192;           // 6 warps
+constexpr int kThreads = 320;           // 10 warps: TMA, MMA, 4 split, 4 drain/epilogue
+constexpr int kChunkKB = 4;             // K-blocks (x32) per TMEM accumulation before promotion
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
 template <int BN, bool SPLIT>
@@ -37,7 +42,7 @@ struct Cfg {
   static constexpr int kTileBytesB = BN * BK * 4;
   static constexpr int kStageBytes = (kTileBytesA + kTileBytesB) * (SPLIT ? 2 : 1);
   static constexpr int kStages = SPLIT ? (BN >= 128 ? 3 : 4) : (BN >= 128 ? 6 : 8);
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   // stage layout: [A raw | A lo | B raw | B lo], every tile 1024-B aligned
   static constexpr int kOffALo = kTileBytesA;
   static constexpr int kOffB = SPLIT ? 2 * kTileBytesA : kTileBytesA;
@@ -175,14 +180,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  // bars: full[S], split[S], empty[S], tmem_full
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 1);
+  // bars: full[S], split[S], empty[S], acc_full[2], acc_empty[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 4);
   const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
-                 empty0 = smem_u32(bars + 2 * C::kStages), tfull = smem_u32(bars + 3 * C::kStages);
+                 empty0 = smem_u32(bars + 2 * C::kStages), afull0 = smem_u32(bars + 3 * C::kStages),
+                 aempty0 = afull0 + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, z = blockIdx.z;
   const int nkb = (ep.k + BK - 1) / BK;
+  const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -192,7 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(split0 + 8 * s, 4);  // one arrive per split warp
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(afull0 + 8 * b, 1);   // tcgen05.commit
+      mbar_init(aempty0 + 8 * b, 4);  // one arrive per drain warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -217,37 +227,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (lane == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::kStages;
-        const uint32_t ph = (kb / C::kStages) & 1;
-        if (SPLIT) mbar_wait(split0 + 8 * s, ph);
-        else mbar_wait(full0 + 8 * s, ph);
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c >= 2) mbar_wait(aempty0 + 8 * buf, ((c >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+        const uint32_t acc = tmem + buf * BN;
+        const int kb_end = min(nkb, (c + 1) * kChunkKB);
+        for (int kb = c * kChunkKB; kb < kb_end; ++kb) {
+          const int s = kb % C::kStages;
+          const uint32_t ph = (kb / C::kStages) & 1;
+          if (SPLIT) mbar_wait(split0 + 8 * s, ph);
+          else mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint32_t st = smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint32_t koff = kk * 32;  // 8 tf32 = 32 B along K inside the swizzle atom
-          const uint64_t ah = desc_sw128(st + koff), bh = desc_sw128(st + C::kOffB + koff);
-          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-          if (SPLIT) {
-            const uint64_t al = desc_sw128(st + C::kOffALo + koff),
-                           bl = desc_sw128(st + C::kOffBLo + koff);
-            mma_tf32(tmem, al, bh, idesc, acc0);  // small terms first
-            mma_tf32(tmem, ah, bl, idesc, 1u);
-            mma_tf32(tmem, ah, bh, idesc, 1u);
-          } else {
-            mma_tf32(tmem, ah, bh, idesc, acc0);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t koff = kk * 32;  // 8 tf32 = 32 B along K inside the swizzle atom
+            const uint64_t ah = desc_sw128(st + koff), bh = desc_sw128(st + C::kOffB + koff);
+            const uint32_t acc0 = (kb > c * kChunkKB || kk > 0) ? 1u : 0u;
+            if (SPLIT) {
+              const uint64_t al = desc_sw128(st + C::kOffALo + koff),
+                             bl = desc_sw128(st + C::kOffBLo + koff);
+              mma_tf32(acc, al, bh, idesc, acc0);  // small terms first
+              mma_tf32(acc, ah, bl, idesc, 1u);
+              mma_tf32(acc, ah, bh, idesc, 1u);
+            } else {
+              mma_tf32(acc, ah, bh, idesc, acc0);
+            }
           }
+          mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
         }
-        mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
+        mma_commit(afull0 + 8 * buf);  // this chunk's partial sum is complete
       }
-      mma_commit(tfull);
     }
-  } else {
-    const int et = threadIdx.x - 64;  // 0..127
-    if (SPLIT) {  // ---- split warps
+  } else if (warp < 6) {
+    if (SPLIT) {  // ---- split warps: raw tile -> (hi in place, lo twin)
+      const int et = threadIdx.x - 64;  // 0..127
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % C::kStages;
         mbar_wait(full0 + 8 * s, (kb / C::kStages) & 1);
@@ -259,31 +276,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(split0 + 8 * s);
       }
     }
-    // ---- epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 = tile rows
-    mbar_wait(tfull, 0);
-    tc_fence_after();
+  } else {
+    // ---- drain + epilogue warps 6..9: warp w owns TMEM lanes 32*(w%4)..+31.
+    // Each K-chunk's TMEM partial is added into fp32 registers with
+    // round-to-nearest adds (promotion): the tensor-core accumulator only ever
+    // sums kChunkKB*32 products, which keeps the long-K error fp32-grade.
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    float* cz = ep.c + z * ep.c_sb;
-    const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
-    const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-      if (row < ep.m) {
+    float racc[BN];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = n0 + c0 + j;
-          if (col < ep.n) {
-            const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
-            float x = v[j];
-            if (ep.accumulate) x = __fadd_rn(cz[off], x);
-            if (bz) x = __fadd_rn(x, bz[col]);
-            x = act_apply(x, ep.act);
-            if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
-            cz[off] = x;
-          }
+    for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
+    }
+    const int row = m0 + q * 32 + lane;
+    if (row < ep.m) {
+      float* cz = ep.c + z * ep.c_sb;
+      const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
+      const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
+#pragma unroll
+      for (int j = 0; j < BN; ++j) {
+        const int col = n0 + j;
+        if (col < ep.n) {
+          const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+          float x = racc[j];
+          if (ep.accumulate) x = __fadd_rn(cz[off], x);
+          if (bz) x = __fadd_rn(x, bz[col]);
+          x = act_apply(x, ep.act);
+          if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
+          cz[off] = x;
         }
       }
     }

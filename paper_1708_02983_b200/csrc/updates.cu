@@ -268,6 +268,37 @@ __global__ void __launch_bounds__(256) k_hogwild_axpy(float* center, const float
   }
 }
 
+// Original EASGD step (trainers/roundrobin.py:120-124): worker step against
+// the center snapshot and the incremental center step with the worker's
+// pre-update weights, both from the same old (w, c), in place.
+template <int V>
+__global__ void __launch_bounds__(256) k_exchange(float* w, const float* __restrict__ g, float* c,
+                                                  int64_t n, float eta, float er) {
+  int64_t nv = n / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (V == 4) {
+      float4 a = ld4rw(w + 4 * i), gg = ld4(g + 4 * i), cc = ld4rw(c + 4 * i), wn, cn;
+      wn.x = worker_rule(a.x, gg.x, cc.x, eta, er); cn.x = incr_rule(cc.x, a.x, er);
+      wn.y = worker_rule(a.y, gg.y, cc.y, eta, er); cn.y = incr_rule(cc.y, a.y, er);
+      wn.z = worker_rule(a.z, gg.z, cc.z, eta, er); cn.z = incr_rule(cc.z, a.z, er);
+      wn.w = worker_rule(a.w, gg.w, cc.w, eta, er); cn.w = incr_rule(cc.w, a.w, er);
+      st4(w + 4 * i, wn);
+      st4(c + 4 * i, cn);
+    } else {
+      float a = w[i], cc = c[i];
+      w[i] = worker_rule(a, g[i], cc, eta, er);
+      c[i] = incr_rule(cc, a, er);
+    }
+  }
+  if (V == 4 && blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    int64_t j = (n & ~int64_t(3)) + threadIdx.x;
+    float a = w[j], cc = c[j];
+    w[j] = worker_rule(a, g[j], cc, eta, er);
+    c[j] = incr_rule(cc, a, er);
+  }
+}
+
 // tree_sum (fabric/collectives.py:25-32): partial[pos] += partial[pos+distance]
 // for distance = 1, 2, 4, ... — the same association as the reference, kept in
 // registers (fully unrolled over the compile-time bound).
@@ -472,4 +503,16 @@ extern "C" int esgd_replica_tree_sum_f32(float* S, const float* W, int64_t ldw, 
   else { ESGD_TREE(64) }
 #undef ESGD_TREE
   return check_launch("esgd_replica_tree_sum_f32");
+}
+
+extern "C" int esgd_exchange_update_f32(float* w, const float* g, float* c, int64_t n, float eta,
+                                        float etarho, esgd_stream_t stream) {
+  ESGD_REQUIRE(n >= 0, ESGD_ERR_SHAPE, "exchange_update: negative length");
+  if (n == 0) return ESGD_OK;
+  ESGD_REQUIRE(w && g && c, ESGD_ERR_INPUT, "exchange_update: null buffer");
+  if (vec_ok({w, g, c}))
+    k_exchange<4><<<stride_grid(n / 4 + 1, 256), 256, 0, ESGD_STREAM(stream)>>>(w, g, c, n, eta, etarho);
+  else
+    k_exchange<1><<<stride_grid(n, 256), 256, 0, ESGD_STREAM(stream)>>>(w, g, c, n, eta, etarho);
+  return check_launch("esgd_exchange_update_f32");
 }

@@ -127,8 +127,10 @@ class DeviceNet:
         self.d_a = self._t(max_act)
         self.d_b = self._t(max_act)
         self.dcol = self._t(max((b * L.hout * L.wout * L.kp for L in self.layers if L.kind == "conv"), default=4))
-        self.scratch = torch.zeros(64 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
+        self.scratch = torch.zeros(256 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # split-K partials of the FFMA GEMM (weight gradients reduce over b*OH*OW)
+        self.gemm_ws = torch.zeros(1 << 22, dtype=torch.float32, device=self.device)
 
     # ---- GEMM routing ------------------------------------------------------
     def _gemm(self, stream, m, n, k, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
@@ -143,7 +145,8 @@ class DeviceNet:
             _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream), "tc_gemm")
         else:
             d = GemmDesc(m, n, k, nb, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
-                         bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0)
+                         bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0,
+                         self.gemm_ws.data_ptr(), self.gemm_ws.numel())
             _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream), "gemm")
 
     # ---- passes ----------------------------------------------------------------

@@ -1,0 +1,53 @@
+"""Per-worker device state for the asynchronous schedules: each worker owns a
+stream, a weight row, a gradient row, optional velocity / snapshot rows and
+its own gradient plan (SplitMix64 stream, workspaces). Workers may live on
+different devices; the center lives on the master device."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ..device import round_up, stream_ptr
+from ..rng import stream_seed
+
+
+class WorkerSlot:
+    def __init__(self, wid: int, problem, init: np.ndarray, device: torch.device, batch_size: int,
+                 seed: int, momentum: bool, snapshot: bool, use_tc: bool = True):
+        self.wid, self.device = wid, device
+        n = init.size
+        self.n, self.ld = n, round_up(n, 64)
+        with torch.cuda.device(device):
+            self.W = torch.zeros((1, self.ld), dtype=torch.float32, device=device)
+            self.W[0, :n] = torch.from_numpy(init).to(device)
+            self.G = torch.zeros_like(self.W)
+            self.V = torch.zeros_like(self.W) if momentum else None
+            self.snap = torch.zeros(self.ld, dtype=torch.float32, device=device) if snapshot else None
+            self.stream = torch.cuda.Stream(device=device)
+            self.plan = problem.bind(device, 1, batch_size, self.ld, use_tc=use_tc)
+            self.plan.set_streams([stream_seed(seed, wid)])
+        self.done = 0
+
+    @property
+    def s(self) -> int:
+        return stream_ptr(self.stream)
+
+    def gradient(self) -> None:
+        with torch.cuda.device(self.device):
+            self.plan.gradient(self.G, self.W, self.s)
+
+    def w(self) -> torch.Tensor:
+        return self.W[0, :self.n]
+
+
+def split_iterations(total: int, workers: int) -> list[int]:
+    """trainers/asynchronous.py:51-54"""
+    base = total // workers
+    return [base + (1 if w < total % workers else 0) for w in range(workers)]
+
+
+def worker_devices(workers: int) -> list[torch.device]:
+    """Workers spread round-robin over the visible GPUs (one process)."""
+    n = torch.cuda.device_count()
+    return [torch.device("cuda", w % n) for w in range(workers)]

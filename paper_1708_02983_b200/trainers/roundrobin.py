@@ -1,0 +1,55 @@
+"""Original EASGD (Alg. 1; reference trainers/roundrobin.py:32-132) on the
+device: one worker per round in strict round-robin order; its worker step
+against the center and the incremental center step with its pre-update
+weights are one fused kernel (esgd_exchange_update_f32). The paper's slow
+baseline, kept for the Table-3 comparison; deterministic and bitwise equal
+to the fp32 reference arithmetic."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..device import require_cuda, stream_ptr
+from ..errors import InputError
+from ..fabric.engine import CATEGORIES
+from ._slots import WorkerSlot
+from .common import Recorder
+from .config import TrainerConfig
+from .records import RunRecord
+
+
+def run_original_easgd(cfg: TrainerConfig, problem, cm=None) -> RunRecord:
+    if cfg.method != "original-easgd":
+        raise InputError(f"not the round-robin method: {cfg.method}")
+    dev = require_cuda()
+    G = cfg.cluster.workers
+    h = cfg.hyper
+    init = np.asarray(problem.init_weights(), dtype=np.float32).reshape(-1)
+    n = init.size
+    slots = [WorkerSlot(w, problem, init, dev, cfg.batch_size, cfg.seed, momentum=False, snapshot=False)
+             for w in range(G)]
+    C = torch.zeros(slots[0].ld, dtype=torch.float32, device=dev)
+    C[:n] = torch.from_numpy(init).to(dev)
+    lib = _lib.load()
+    rec = Recorder(problem, cfg.eval_every, cfg.iterations)
+    s = stream_ptr()
+    elapsed = 0.0
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record()
+    for t in range(cfg.iterations):
+        sl = slots[t % G]
+        sl.plan.gradient(sl.G, sl.W, s)
+        _lib.check(lib.esgd_exchange_update_f32(sl.W.data_ptr(), sl.G.data_ptr(), C.data_ptr(), n,
+                                                h.eta32, h.etarho32, s))
+        if rec.due(t + 1):
+            t1.record()
+            t1.synchronize()
+            elapsed += t0.elapsed_time(t1) / 1e3
+            rec.record(t + 1, elapsed, C[:n])
+            t0.record()
+    return rec.build(cfg.method, elapsed, C[:n].cpu().numpy(), breakdown={c: 0.0 for c in CATEGORIES},
+                     worker_weights=[sl.W[0, :n].cpu().numpy() for sl in slots],
+                     engine_info={"engine": "cuda"})

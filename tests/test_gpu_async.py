@@ -1,0 +1,74 @@
+"""Async (FCFS master), Hogwild (lock-free streams) and original EASGD on the
+B200. Round-robin is deterministic and bitwise; async/Hogwild are racing by
+design, so parity is statistical (convergence / distance to optimum,
+reference trainers/hogwild.py:1-16)."""
+
+import numpy as np
+import pytest
+
+from oracle import esgd_oracle as O
+from paper_1708_02983_b200 import HyperParams, make_config, run_trainer
+from paper_1708_02983_b200.trainers import QuadraticProblem
+
+pytestmark = pytest.mark.gpu
+HY = HyperParams(eta=0.1, rho=0.5, mu=0.9)
+
+
+def _oracle_roundrobin(prob, G, T, eta, rho, seed):
+    rngs = [O.worker_rng(seed, w) for w in range(G)]
+    init = prob.init_weights()
+    W = [init.copy() for _ in range(G)]
+    C = init.copy()
+    for t in range(T):
+        j = t % G
+        g = prob.gradient(W[j], rngs[j], 1)
+        w_old = W[j]
+        W[j] = O.easgd_worker_step(w_old, g, C, eta, rho)
+        C = O.easgd_center_incremental(C, w_old, eta, rho)
+    return C, W
+
+
+def test_original_easgd_bitwise_vs_oracle():
+    prob = QuadraticProblem.random(130, seed=2)
+    rec = run_trainer(make_config("original-easgd", workers=3, iterations=60, hyper=HY, seed=4), prob)
+    C, W = _oracle_roundrobin(O.QuadProblem.random(130, 2, np.float32), 3, 60, 0.1, 0.5, 4)
+    assert np.array_equal(rec.final_weights, C)
+    assert np.array_equal(np.stack(rec.final_worker_weights), np.stack(W))
+
+
+def test_async_single_worker_equals_roundrobin():
+    """P=1: async-easgd collapses onto original EASGD (tests/test_trainers.py:33-38)."""
+    prob = QuadraticProblem.random(64, seed=3)
+    a = run_trainer(make_config("async-easgd", workers=1, iterations=80, hyper=HY, seed=3), prob)
+    b = run_trainer(make_config("original-easgd", workers=1, iterations=80, hyper=HY, seed=3), prob)
+    assert np.array_equal(a.final_weights, b.final_weights)
+
+
+@pytest.mark.parametrize("method", ["async-easgd", "async-measgd", "async-sgd", "async-msgd"])
+def test_async_converges(method):
+    prob = QuadraticProblem.random(50, seed=8)
+    hy = HyperParams(eta=0.05, rho=0.5, mu=0.5)
+    rec = run_trainer(make_config(method, workers=4, iterations=2000, hyper=hy, seed=9), prob)
+    assert prob.distance_to_optimum(rec.final_weights) < 1e-3, method
+
+
+@pytest.mark.parametrize("method,workers", [("hogwild-easgd", 16), ("hogwild-easgd", 8), ("hogwild-sgd", 8)])
+def test_hogwild_converges_many_streams(method, workers):
+    """8 racing streams as in the reference (tests/test_threaded.py:83-89);
+    hogwild-sgd's stale full-gradient steps diverge once eta*L*workers > 2,
+    so it keeps the reference's worker count, while the elastic variant is
+    also run with 16 streams."""
+    prob = QuadraticProblem.random(50, seed=13)
+    rec = run_trainer(make_config(method, workers=workers, iterations=4000, hyper=HY, seed=14), prob)
+    assert prob.distance_to_optimum(rec.final_weights) < 1e-3
+
+
+def test_async_measgd_statistical_parity_with_reference(golden):
+    """same problem / budget as the reference's simulated run: both land near
+    the optimum (the FCFS orders differ by construction)."""
+    g = golden("trainers")
+    prob = QuadraticProblem(g["quad_target"], g["quad_curv"])
+    rec = run_trainer(make_config("async-measgd", workers=4, iterations=400, hyper=HY, seed=5), prob)
+    ours = prob.distance_to_optimum(rec.final_weights)
+    ref = float(g["quad_async-measgd_dist"][0])
+    assert ours < max(10 * ref, 1e-2), (ours, ref)

@@ -75,8 +75,8 @@ def test_hogwild_single_stream_exact():
     rng = np.random.default_rng(1)
     n = 4099
     c0, w0, s0 = (rng.standard_normal(n).astype(np.float32) for _ in range(3))
-    c = dev(c0)
-    engine.hogwild_elastic_apply(c, dev(w0), dev(s0), float(np.float32(0.05 * 0.25)))
+    c, wd, sd = dev(c0), dev(w0), dev(s0)
+    engine.hogwild_elastic_apply(c, wd, sd, float(np.float32(0.05 * 0.25)))
     expect = c0.copy()
     O.hogwild_apply(expect, (0.05 * 0.25) * (w0 - s0))
     assert np.array_equal(host(c), expect)
@@ -115,9 +115,10 @@ def test_sample_batch_gathers_and_advances_counter():
     ticket = torch.zeros(nrep, dtype=torch.int32, device="cuda")
     xo = torch.zeros((nrep, b * d), device="cuda")
     yo = torch.zeros((nrep, b), dtype=torch.int32, device="cuda")
+    Xd, Yd = dev(X), dev(Y, torch.int32)  # keep alive: launches are asynchronous
     for rnd in range(2):
         _lib.call("esgd_sample_batch_f32", xo.data_ptr(), xo.stride(0), yo.data_ptr(), None,
-                  dev(X).data_ptr(), dev(Y, torch.int32).data_ptr(), n, d, state.data_ptr(),
+                  Xd.data_ptr(), Yd.data_ptr(), n, d, state.data_ptr(),
                   ticket.data_ptr(), b, nrep, stream_ptr())
         torch.cuda.synchronize()
         for r in range(nrep):
@@ -136,8 +137,9 @@ def test_softmax_xent_vs_reference(golden):
     lg = dev(logits)
     dl = torch.empty_like(lg)
     rl = torch.empty(rows, device="cuda")
+    lab = dev(labels, torch.int32)
     _lib.call("esgd_softmax_xent_f32", dl.data_ptr(), rl.data_ptr(), lg.data_ptr(), cols, rows * cols,
-              dev(labels, torch.int32).data_ptr(), rows, rows, cols, 1, None, stream_ptr())
+              lab.data_ptr(), rows, rows, cols, 1, None, stream_ptr())
     assert rel_err(host(dl), g["xent_dlogits"]) < 1e-6
     assert abs(float(host(rl).astype(np.float64).mean()) - g["xent_loss"][0]) < 1e-6
 
@@ -146,25 +148,30 @@ def _gemm_ref(A, B):
     return A.astype(np.float64) @ B.astype(np.float64)
 
 
-@pytest.mark.parametrize("m,n,k,batch", [(1, 1, 1, 1), (64, 10, 500, 2), (130, 70, 33, 3), (257, 500, 800, 1)])
-def test_ffma_gemm_strided(m, n, k, batch):
+@pytest.mark.parametrize("m,n,k,batch", [(1, 1, 1, 1), (64, 10, 500, 2), (130, 70, 33, 3), (257, 500, 800, 1),
+                                         (20, 25, 36864, 2), (50, 500, 4096, 1)])
+@pytest.mark.parametrize("split", [False, True])
+def test_ffma_gemm_strided(m, n, k, batch, split):
     rng = np.random.default_rng(m * n + k)
     A = rng.standard_normal((batch, m, k)).astype(np.float32)
     B = rng.standard_normal((batch, n, k)).astype(np.float32)  # stored N x K -> B(k,n) stride (1, k)
     bias = rng.standard_normal((batch, n)).astype(np.float32)
     Ad, Bd, bd = dev(A), dev(B), dev(bias)
     Cd = torch.zeros((batch, m, n), device="cuda")
+    ws = torch.zeros(1 << 20, device="cuda")
     d = _lib.GemmDesc(m, n, k, batch, Ad.data_ptr(), k, 1, m * k, Bd.data_ptr(), 1, k, n * k,
-                      Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, None, 1, 0)
+                      Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, None, 1, 0,
+                      ws.data_ptr() if split else None, ws.numel() if split else 0)
     _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream_ptr()))
     for z in range(batch):
         ref = np.maximum(_gemm_ref(A[z], B[z].T) + bias[z], 0)
-        assert rel_err(host(Cd[z]), ref) < 1e-6
+        # sequential fp32 accumulation: error grows ~sqrt(k) without split-K
+        assert rel_err(host(Cd[z]), ref) < (2e-6 if (split or k <= 1024) else 1e-5)
 
 
 @pytest.mark.parametrize("m,n,k,batch", [(128, 64, 32, 1), (300, 50, 500, 2), (1024, 192, 1600, 1),
                                          (4096, 128, 363, 1), (257, 1000, 4096, 1), (129, 20, 25, 3)])
-@pytest.mark.parametrize("precision,tol", [(3, 2e-6), (1, 5e-3)])
+@pytest.mark.parametrize("precision,tol", [(3, 3e-6), (1, 5e-3)])
 def test_tcgen05_gemm(m, n, k, batch, precision, tol):
     """tcgen05 kind::tf32 GEMM: 3xTF32 reaches fp32-grade error; plain TF32 ~1e-3."""
     rng = np.random.default_rng(m + n + k)
@@ -193,13 +200,15 @@ def test_im2col_col2im_adjoint_and_oracle():
     K = c * k * k
     kp = (K + 3) // 4 * 4
     col = torch.zeros((n * oh * ow, kp), device="cuda")
-    _lib.call("esgd_im2col_f32", col.data_ptr(), kp, 0, dev(x).data_ptr(), _lib.nchw(n, c, h, w), 0,
+    xd = dev(x)
+    _lib.call("esgd_im2col_f32", col.data_ptr(), kp, 0, xd.data_ptr(), _lib.nchw(n, c, h, w), 0,
               k, k, s, p, oh, ow, 1, stream_ptr())
     ref, _, _ = O._im2col(x, k, s, p)
     assert np.array_equal(host(col)[:, :K], ref)
     dcol = rng.standard_normal((n * oh * ow, kp)).astype(np.float32)
     dx = torch.zeros((n, c, h, w), device="cuda")
-    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dev(dcol).data_ptr(), kp, 0,
+    dcd = dev(dcol)
+    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dcd.data_ptr(), kp, 0,
               k, k, s, p, oh, ow, None, 1, stream_ptr())
     exp = O._col2im(dcol[:, :K].copy(), (n, c, h, w), k, s, p, oh, ow)
     assert np.array_equal(host(dx), exp)
@@ -213,12 +222,14 @@ def test_maxpool_fwd_bwd_vs_oracle():
     x[0, 0, :4, :4] = 1.0  # ties: first max in scan order wins
     y = torch.zeros((n, c, oh, ow), device="cuda")
     am = torch.zeros((n, c, oh, ow), dtype=torch.int32, device="cuda")
-    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), dev(x).data_ptr(),
+    xd = dev(x)
+    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), xd.data_ptr(),
               _lib.nchw(n, c, h, w), 0, k, s, p, 1, stream_ptr())
     ey, ea = O._maxpool(x, k, s, p)
     assert np.array_equal(host(y), ey) and np.array_equal(host(am), ea)
     dy = rng.standard_normal((n, c, oh, ow)).astype(np.float32)
     dx = torch.zeros((n, c, h, w), device="cuda")
-    _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dev(dy).data_ptr(),
+    dyd = dev(dy)
+    _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dyd.data_ptr(),
               _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), None, k, s, p, 1, stream_ptr())
     assert np.array_equal(host(dx), O._maxpool_bwd(dy, ea, (n, c, h, w)))
