@@ -148,11 +148,16 @@ typedef struct {
 int esgd_gemm_f32(const esgd_gemm_desc* desc, esgd_stream_t stream);
 
 /* Tensor-core GEMM (tcgen05.mma kind::tf32, TMA-fed, accumulator in TMEM)
- * with 3xTF32 error compensation (hi*hi + hi*lo + lo*hi), i.e. fp32-grade
- * results. Operands are K-major fp32: A is m x k (row pitch lda floats),
- * B is n x k (row pitch ldb floats); C = A . B^T (+bias, act) written with
- * strides (c_sm, c_sn). lda/ldb must be multiples of 4; pointers 16B aligned.
- * Batched over `batch` with element strides a_sb, b_sb, c_sb.              */
+ * with 3xTF32 error compensation (hi*hi + hi*lo + lo*hi) and per-128-K
+ * promotion of the TMEM partial sums into fp32 registers: fp32-grade
+ * results. C[z] = A[z] . B[z] (+bias, act, mask), C (m x n) with strides
+ * (c_sm, c_sn). Operand layouts (fp32):
+ *   a_major 0: A[m*lda + k] (K-major)   1: A[k*lda + m] (M-major)
+ *   b_major 0: B[n*ldb + k] (K-major)   1: B[k*ldb + n] (N-major)
+ * lda/ldb multiples of 4, A/B 16-B aligned (TMA). Batched over `batch` with
+ * element strides a_sb, b_sb, c_sb. With `ws` (ws_floats floats of device
+ * scratch) small-output / long-K problems split K across CTAs and combine
+ * the partials in a fixed order (deterministic).                           */
 typedef struct {
   int32_t m, n, k, batch;
   const float* a; int64_t lda, a_sb;
@@ -163,6 +168,9 @@ typedef struct {
   int32_t act;
   int32_t accumulate;
   int32_t precision; /* 3 = 3xTF32 (fp32-grade, default), 1 = plain TF32 */
+  int32_t a_major, b_major;
+  float* ws;
+  int64_t ws_floats;
 } esgd_tc_gemm_desc;
 int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* desc, esgd_stream_t stream);
 

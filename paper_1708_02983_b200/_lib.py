@@ -44,6 +44,7 @@ class TcGemmDesc(C.Structure):
         ("bias", vp), ("bias_sb", i64),
         ("mask", vp), ("mask_sm", i64), ("mask_sn", i64), ("mask_sb", i64),
         ("act", i32), ("accumulate", i32), ("precision", i32),
+        ("a_major", i32), ("b_major", i32), ("ws", vp), ("ws_floats", i64),
     ]
 
 

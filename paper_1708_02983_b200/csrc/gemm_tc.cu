@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 namespace esgd {
 namespace tc {
 
@@ -100,11 +102,28 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-// instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B
-__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+// MN-major tf32 operands: UMMA accepts only the "128B swizzle with 32-byte
+// atomicity" layout (SWIZZLE_128B_BASE32B; CUTLASS sm100 builder: "for
+// mn-major tf32 operands, SW128_32B is the only available smem layout"),
+// loaded by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B. Atoms are 32 MN
+// elements (128 B) x 4 K rows; each TMA box of 32(MN) x 32(K) lands as 4 KB,
+// so K-atoms are SBO = 512 B apart and MN-atoms LBO = 4096 B.
+__device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(4096 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+// instruction descriptor: kind::tf32, fp32 accumulate, A/B major per flag
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n, bool a_mn, bool b_mn) {
   return (1u << 4)                      // c_format = F32
          | (2u << 7)                    // a_format = TF32
          | (2u << 10)                   // b_format = TF32
+         | ((a_mn ? 1u : 0u) << 15)     // a_major: 1 = MN-major
+         | ((b_mn ? 1u : 0u) << 16)     // b_major
          | ((uint32_t)(n >> 3) << 17)   // N >> 3
          | ((uint32_t)(m >> 4) << 24);  // M >> 4
 }
@@ -150,7 +169,38 @@ struct Epi {
   const float* bias; int64_t bias_sb;
   const float* mask; int64_t mask_sm, mask_sn, mask_sb;
   int act, accumulate, m, n, k;
+  float* ws;        // split-K partials [batch][splits][m][n]
+  int splits, kb_per_split;
 };
+
+__device__ __forceinline__ float epi_apply(const Epi& ep, float x, int z, int row, int col, int64_t off,
+                                           const float* cz) {
+  const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
+  const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
+  if (ep.accumulate) x = __fadd_rn(cz[off], x);
+  if (bz) x = __fadd_rn(x, bz[col]);
+  x = act_apply(x, ep.act);
+  if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
+  return x;
+}
+
+// TMA of one operand tile for k-block kb: K-major = one box (32 K x rows);
+// MN-major = rows/32 boxes of (32 MN x 32 K), 4 KB apart.
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint32_t bar, int kb,
+                                             int r0, int z) {
+  if (!MN) {
+    tma_load_3d(dst, map, bar, kb * BK, r0, z);
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS / 32; ++j) tma_load_3d(dst + j * 4096, map, bar, r0 + 32 * j, kb * BK, z);
+  }
+}
+
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t tile, int kk) {
+  return MN ? desc_sw128_mn(tile + kk * 1024) : desc_sw128(tile + kk * 32);
+}
 
 // split one landed tile: hi = tf32-truncated x (in place), lo = x - hi
 __device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, int bytes, int tid) {
@@ -172,7 +222,7 @@ __device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, int bytes,
   }
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               Epi ep) {
@@ -187,8 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                  aempty0 = afull0 + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN, z = blockIdx.z;
-  const int nkb = (ep.k + BK - 1) / BK;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int z = blockIdx.z / ep.splits, slice = blockIdx.z % ep.splits;
+  const int nkb_all = (ep.k + BK - 1) / BK;
+  const int kb0 = slice * ep.kb_per_split;
+  const int nkb = max(0, min(nkb_all - kb0, ep.kb_per_split));  // k-blocks of this slice
   const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
 
   if (warp == 0 && lane == 0) {
@@ -222,13 +275,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kb >= C::kStages) mbar_wait(empty0 + 8 * s, ((kb / C::kStages) - 1) & 1);
         uint8_t* st = smem + s * C::kStageBytes;
         mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
-        tma_load_3d(smem_u32(st), &map_a, full0 + 8 * s, kb * BK, m0, z);
-        tma_load_3d(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, kb * BK, n0, z);
+        load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, kb0 + kb, m0, z);
+        load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, kb0 + kb, n0, z);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
-      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, AMN, BMN);
       for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
         if (c >= 2) mbar_wait(aempty0 + 8 * buf, ((c >> 1) - 1) & 1);
@@ -244,12 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t koff = kk * 32;  // 8 tf32 = 32 B along K inside the swizzle atom
-            const uint64_t ah = desc_sw128(st + koff), bh = desc_sw128(st + C::kOffB + koff);
+            // K-major: 8 tf32 = 32 B along K inside the swizzle atom;
+            // MN-major: one 8-row K-atom (1024 B) per instruction
+            const uint64_t ah = op_desc<AMN>(st, kk), bh = op_desc<BMN>(st + C::kOffB, kk);
             const uint32_t acc0 = (kb > c * kChunkKB || kk > 0) ? 1u : 0u;
             if (SPLIT) {
-              const uint64_t al = desc_sw128(st + C::kOffALo + koff),
-                             bl = desc_sw128(st + C::kOffBLo + koff);
+              const uint64_t al = op_desc<AMN>(st + C::kOffALo, kk),
+                             bl = op_desc<BMN>(st + C::kOffBLo, kk);
               mma_tf32(acc, al, bh, idesc, acc0);  // small terms first
               mma_tf32(acc, ah, bl, idesc, 1u);
               mma_tf32(acc, ah, bh, idesc, 1u);
@@ -302,20 +356,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int row = m0 + q * 32 + lane;
     if (row < ep.m) {
-      float* cz = ep.c + z * ep.c_sb;
-      const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
-      const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
+      if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
+        float* P = ep.ws + ((int64_t)z * ep.splits + slice) * ep.m * ep.n + (int64_t)row * ep.n;
 #pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const int col = n0 + j;
-        if (col < ep.n) {
-          const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
-          float x = racc[j];
-          if (ep.accumulate) x = __fadd_rn(cz[off], x);
-          if (bz) x = __fadd_rn(x, bz[col]);
-          x = act_apply(x, ep.act);
-          if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
-          cz[off] = x;
+        for (int j = 0; j < BN; ++j)
+          if (n0 + j < ep.n) P[n0 + j] = racc[j];
+      } else {
+        float* cz = ep.c + z * ep.c_sb;
+#pragma unroll
+        for (int j = 0; j < BN; ++j) {
+          const int col = n0 + j;
+          if (col < ep.n) {
+            const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+            cz[off] = epi_apply(ep, racc[j], z, row, col, off, cz);
+          }
         }
       }
     }
@@ -325,6 +379,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+  }
+}
+
+// combine split-K partials in slice order (deterministic), then the epilogue
+__global__ void __launch_bounds__(256) k_tc_reduce(Epi ep) {
+  const int64_t mn = (int64_t)ep.m * ep.n;
+  const int z = blockIdx.y;
+  float* cz = ep.c + z * ep.c_sb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+    const float* P = ep.ws + (int64_t)z * ep.splits * mn + e;
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+    int s = 0;
+    for (; s + 3 < ep.splits; s += 4) {
+      v0 = __fadd_rn(v0, P[s * mn]); v1 = __fadd_rn(v1, P[(s + 1) * mn]);
+      v2 = __fadd_rn(v2, P[(s + 2) * mn]); v3 = __fadd_rn(v3, P[(s + 3) * mn]);
+    }
+    for (; s < ep.splits; ++s) v0 = __fadd_rn(v0, P[s * mn]);
+    const int row = (int)(e / ep.n), col = (int)(e % ep.n);
+    const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+    cz[off] = epi_apply(ep, __fadd_rn(__fadd_rn(v0, v1), __fadd_rn(v2, v3)), z, row, col, off, cz);
   }
 }
 
@@ -340,41 +414,70 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3-D map over a K-major operand: dims (k, rows, batch), box (32, box_rows, 1)
+// 3-D map over an operand. K-major: dims (k, rows, batch), box (32, box_rows, 1).
+// MN-major: dims (rows, k, batch) with rows contiguous, box (32, 32, 1).
 int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64_t ld,
-             int64_t batch, int64_t sb, int box_rows) {
+             int64_t batch, int64_t sb, int box_rows, bool mn_major) {
   auto enc = get_encode();
   ESGD_REQUIRE(enc, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)batch};
-  int64_t bstride = batch > 1 ? sb : ld * rows;
+  const int64_t inner = mn_major ? rows : k, outer = mn_major ? k : rows;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
+  int64_t bstride = batch > 1 ? sb : ld * outer;
   bstride = (bstride + 3) & ~int64_t(3);
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
-  cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {32, (cuuint32_t)(mn_major ? BK : box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   ESGD_REQUIRE(r == CUDA_SUCCESS, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ESGD_OK;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool AMN, bool BMN>
 int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   using C = Cfg<BN, SPLIT>;
   // per-device attribute; cheap, and legal while a stream is being captured
-  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT, AMN, BMN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: smem attribute: %s", cudaGetErrorString(e));
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM);
+  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN);
   if (rc) return rc;
-  rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN);
+  rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN, BMN);
   if (rc) return rc;
+  const int nkb = (d->k + BK - 1) / BK;
+  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
+  // split K when the output tiles cannot fill the 148 SMs (weight gradients
+  // reduce over every pixel of the batch): ~2 waves, >= 4 chunks per slice
+  int splits = 1;
+  if (d->ws && tiles < kNumSMs && nkb >= 2 * kChunkKB) {
+    splits = (2 * kNumSMs) / tiles;
+    splits = std::min(splits, nkb / (2 * kChunkKB));
+    splits = std::min(splits, 128);
+    while (splits > 1 && (int64_t)splits * d->m * d->n * d->batch > d->ws_floats) --splits;
+    if ((int64_t)d->batch * splits > 65535) splits = 1;
+    if (splits < 1) splits = 1;
+  }
+  int kbps = (nkb + splits - 1) / splits;
+  kbps = (kbps + kChunkKB - 1) / kChunkKB * kChunkKB;
+  splits = (nkb + kbps - 1) / kbps;
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
-         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k};
-  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch);
-  k_tc_gemm<BN, SPLIT><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, ep);
+         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps};
+  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch * splits);
+  k_tc_gemm<BN, SPLIT, AMN, BMN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, ep);
+  if (splits > 1) {
+    dim3 rg(stride_grid((int64_t)d->m * d->n, 256, 8), d->batch);
+    k_tc_reduce<<<rg, 256, 0, st>>>(ep);
+  }
   return check_launch("esgd_tc_gemm_f32");
+}
+
+template <int BN, bool SPLIT>
+int launch_major(const esgd_tc_gemm_desc* d, cudaStream_t st) {
+  if (d->a_major) return d->b_major ? launch<BN, SPLIT, true, true>(d, st) : launch<BN, SPLIT, true, false>(d, st);
+  return d->b_major ? launch<BN, SPLIT, false, true>(d, st) : launch<BN, SPLIT, false, false>(d, st);
 }
 
 }  // namespace tc
@@ -390,8 +493,9 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
   ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "tc_gemm: unknown activation");
   if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
   ESGD_REQUIRE(d->k >= 1 && d->a && d->b && d->c, ESGD_ERR_INPUT, "tc_gemm: null operand");
-  ESGD_REQUIRE(d->lda >= d->k && d->ldb >= d->k && (d->lda & 3) == 0 && (d->ldb & 3) == 0,
-               ESGD_ERR_SHAPE, "tc_gemm: lda/ldb must be >= k and multiples of 4 (TMA 16-B strides)");
+  ESGD_REQUIRE(d->lda >= (d->a_major ? d->m : d->k) && d->ldb >= (d->b_major ? d->n : d->k) &&
+                   (d->lda & 3) == 0 && (d->ldb & 3) == 0,
+               ESGD_ERR_SHAPE, "tc_gemm: lda/ldb must cover the contiguous dim and be multiples of 4 (TMA 16-B strides)");
   ESGD_REQUIRE(aligned16(d->a) && aligned16(d->b), ESGD_ERR_INPUT, "tc_gemm: A/B must be 16-B aligned");
   ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
                "tc_gemm: batch strides must be multiples of 4");
@@ -399,6 +503,6 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
                "tc_gemm: grid too large");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool split = d->precision == 3;
-  if (d->n <= 64) return split ? tc::launch<64, true>(d, st) : tc::launch<64, false>(d, st);
-  return split ? tc::launch<128, true>(d, st) : tc::launch<128, false>(d, st);
+  if (d->n <= 64) return split ? tc::launch_major<64, true>(d, st) : tc::launch_major<64, false>(d, st);
+  return split ? tc::launch_major<128, true>(d, st) : tc::launch_major<128, false>(d, st);
 }

@@ -131,23 +131,41 @@ class DeviceNet:
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
         # split-K partials of the FFMA GEMM (weight gradients reduce over b*OH*OW)
         self.gemm_ws = torch.zeros(1 << 22, dtype=torch.float32, device=self.device)
+        self.tc_ws = torch.zeros(1 << 23, dtype=torch.float32, device=self.device)
+        # conv weights whose row (K) is not a multiple of 4 floats get a padded
+        # copy each round so the forward GEMM can take them through TMA
+        self.wpad = [self._t(L.cout * L.kp) if (L.kind == "conv" and L.k % 4) else None for L in self.layers]
+        self.tc_calls = self.ffma_calls = 0
 
     # ---- GEMM routing ------------------------------------------------------
     def _gemm(self, stream, m, n, k, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
               bias=None, bias_sb=0, mask=None, mask_sm=0, mask_sn=0, mask_sb=0, act=0, pre=None):
+        """C = act(A.B + bias) (*mask). Routed to the tcgen05 3xTF32 kernel when
+        both operands have a unit-stride dim with 16-B-aligned pitch (either
+        K-major or MN-major) and the problem is big enough; else FFMA."""
         nb = self.nrep
-        tc_ok = (self.use_tc and pre is None and a_sk == 1 and b_sk == 1 and a_sm % 4 == 0 and
-                 b_sn % 4 == 0 and a % 16 == 0 and bm % 16 == 0 and m >= 128 and
-                 (nb == 1 or (a_sb % 4 == 0 and b_sb % 4 == 0)) and m * n * k >= TC_MIN_FLOPS)
-        if tc_ok:
-            d = TcGemmDesc(m, n, k, nb, a, a_sm, a_sb, bm, b_sn, b_sb, c, c_sm, c_sn, c_sb,
-                           bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, act, 0, self.precision)
+        tc = None
+        if self.use_tc and pre is None and m * n * k >= TC_MIN_FLOPS and a % 16 == 0 and bm % 16 == 0:
+            a_major = 0 if a_sk == 1 else (1 if a_sm == 1 else None)
+            b_major = 0 if b_sk == 1 else (1 if b_sn == 1 else None)
+            if a_major is not None and b_major is not None:
+                lda = a_sm if a_major == 0 else a_sk
+                ldb = b_sn if b_major == 0 else b_sk
+                if lda % 4 == 0 and ldb % 4 == 0 and (nb == 1 or (a_sb % 4 == 0 and b_sb % 4 == 0)):
+                    tc = (a_major, b_major, lda, ldb)
+        if tc is not None:
+            a_major, b_major, lda, ldb = tc
+            d = TcGemmDesc(m, n, k, nb, a, lda, a_sb, bm, ldb, b_sb, c, c_sm, c_sn, c_sb,
+                           bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, act, 0, self.precision,
+                           a_major, b_major, self.tc_ws.data_ptr(), self.tc_ws.numel())
             _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream), "tc_gemm")
+            self.tc_calls += 1
         else:
             d = GemmDesc(m, n, k, nb, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
                          bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0,
                          self.gemm_ws.data_ptr(), self.gemm_ws.numel())
             _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream), "gemm")
+            self.ffma_calls += 1
 
     # ---- passes ----------------------------------------------------------------
     def forward(self, W: torch.Tensor, stream: int, x: torch.Tensor | None = None) -> torch.Tensor:
@@ -169,9 +187,16 @@ class DeviceNet:
                 _lib.check(lib.esgd_im2col_f32(col.data_ptr(), L.kp, col.stride(0), cur, cur_d, cur_sb,
                                                lay.k, lay.k, lay.stride, lay.pad, L.hout, L.wout, nb,
                                                stream), "im2col")
+                w_ptr, w_pitch, w_sb = wp + 4 * L.w_off, L.k, ldw
+                if self.wpad[i] is not None:
+                    pw = self.wpad[i]
+                    _lib.check(lib.esgd_copy4_f32(pw.data_ptr(), Tensor4(1, L.cout, 1, L.k, 0, L.kp, 0, 1),
+                                                  pw.stride(0), w_ptr, Tensor4(1, L.cout, 1, L.k, 0, L.k, 0, 1),
+                                                  ldw, nb, stream), "pad_weights")
+                    w_ptr, w_pitch, w_sb = pw.data_ptr(), L.kp, pw.stride(0)
                 self._gemm(stream, b * L.hout * L.wout, L.cout, L.k,
                            col.data_ptr(), L.kp, 1, col.stride(0),
-                           wp + 4 * L.w_off, 1, L.k, ldw,
+                           w_ptr, 1, w_pitch, w_sb,
                            o, L.cout, 1, o_sb, bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act)
                 cur_d = nhwc(b, L.cout, L.hout, L.wout)
                 cur_flat = False

@@ -184,7 +184,8 @@ def test_tcgen05_gemm(m, n, k, batch, precision, tol):
     Ad, Bd, bd = dev(A), dev(B), dev(bias)
     Cd = torch.zeros((batch, m, n), device="cuda")
     d = _lib.TcGemmDesc(m, n, k, batch, Ad.data_ptr(), kp, m * kp, Bd.data_ptr(), kp, n * kp,
-                        Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, 0, 0, precision)
+                        Cd.data_ptr(), n, 1, m * n, bd.data_ptr(), n, None, 0, 0, 0, 0, 0, precision,
+                        0, 0, None, 0)
     _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
     torch.cuda.synchronize()
     for z in range(batch):
@@ -233,3 +234,35 @@ def test_maxpool_fwd_bwd_vs_oracle():
     _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dyd.data_ptr(),
               _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), None, k, s, p, 1, stream_ptr())
     assert np.array_equal(host(dx), O._maxpool_bwd(dy, ea, (n, c, h, w)))
+
+
+@pytest.mark.parametrize("a_major,b_major", [(0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("m,n,k,batch", [(200, 96, 300, 2), (64, 363, 38720, 1), (9216 // 8, 4096 // 8, 128, 1)])
+def test_tcgen05_gemm_mn_major_and_split_k(a_major, b_major, m, n, k, batch):
+    """MN-major operands (weight-gradient / N-major weight layouts) and the
+    deterministic split-K path (long reductions over pixels)."""
+    rng = np.random.default_rng(m * 7 + n + k)
+    A = rng.standard_normal((batch, m, k)).astype(np.float32)
+    B = rng.standard_normal((batch, n, k)).astype(np.float32)
+    As = np.ascontiguousarray(A.transpose(0, 2, 1)) if a_major else A
+    Bs = np.ascontiguousarray(B.transpose(0, 2, 1)) if b_major else B
+    lda = m if a_major else k
+    ldb = n if b_major else k
+    if lda % 4 or ldb % 4:
+        pytest.skip("TMA needs 16-B pitches")
+    Ad, Bd = dev(As), dev(Bs)
+    Cd = torch.zeros((batch, m, n), device="cuda")
+    ws = torch.zeros(1 << 24, device="cuda")
+    d = _lib.TcGemmDesc(m, n, k, batch, Ad.data_ptr(), lda, m * k, Bd.data_ptr(), ldb, n * k,
+                        Cd.data_ptr(), n, 1, m * n, None, 0, None, 0, 0, 0, 0, 0, 3,
+                        a_major, b_major, ws.data_ptr(), ws.numel())
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    torch.cuda.synchronize()
+    for z in range(batch):
+        ref = _gemm_ref(A[z], B[z].T)
+        assert rel_err(host(Cd[z]), ref) < 3e-6, (z, rel_err(host(Cd[z]), ref))
+    # determinism of the split-K combine
+    C2 = torch.zeros_like(Cd)
+    d.c = C2.data_ptr()
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    assert torch.equal(Cd, C2)
