@@ -210,20 +210,29 @@ typedef struct {
   int64_t sn, sc, sh, sw;
 } esgd_tensor4;
 
-/* im2col: col[(img*OH*OW + oh*OW + ow) * ldc + (ci*kh + ky)*kw + kx] =
- *   x(img, ci, oh*stride - pad + ky, ow*stride - pad + kx) (0 outside).
- * Columns k..ldc-1 are zero-filled. Batched over `batch` (x_sb, col_sb).   */
-int esgd_im2col_f32(float* col, int64_t ldc, int64_t col_sb, const float* x, esgd_tensor4 xd,
-                    int64_t x_sb, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
-                    int32_t oh, int32_t ow, int32_t batch, esgd_stream_t stream);
+/* im2col: the column element (pix, k), pix = (img*OH + oh)*OW + ow and
+ * k = (ci*kh + ky)*kw + kx, is col[pix*col_sp + k*col_sk] =
+ * x(img, ci, oh*stride - pad + ky, ow*stride - pad + kx) (0 outside).
+ * Layouts: (col_sp, col_sk) = (>=K, 1) row-major, or (1, >=pixels)
+ * transposed (the engine's; TMA-friendly for the weight-gradient GEMM).
+ * Batched over `batch` (x_sb, col_sb).                                     */
+int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64_t col_sb, const float* x,
+                    esgd_tensor4 xd, int64_t x_sb, int32_t kh, int32_t kw, int32_t stride,
+                    int32_t pad, int32_t oh, int32_t ow, int32_t batch, esgd_stream_t stream);
 
-/* col2im (adjoint of im2col, gather form, fixed order): dx(img,ci,y,x) =
- * sum over (ky,kx) of dcol rows hitting (y,x); optional mask multiplies the
- * result by (mask>0) with mask laid out like dx (relu-grad).              */
-int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol, int64_t ldc,
-                    int64_t col_sb, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
-                    int32_t oh, int32_t ow, const float* mask, int32_t batch,
+/* col2im (adjoint of im2col, gather form, fixed (ky, kx) order): dx(img,ci,y,x)
+ * = sum of the dcol entries im2col took from (y,x); optional mask multiplies
+ * the result by (mask>0) with mask laid out like dx (relu-grad).           */
+int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol, int64_t col_sp,
+                    int64_t col_sk, int64_t col_sb, int32_t kh, int32_t kw, int32_t stride,
+                    int32_t pad, int32_t oh, int32_t ow, const float* mask, int32_t batch,
                     esgd_stream_t stream);
+
+/* row sums: out[z*out_sb + r] = sum_{j<cols} x[z*x_sb + r*ld + j] (conv bias
+ * gradients over channel-major activations; network.py:195 generalised).
+ * Deterministic fixed-order reduction; scratch >= 64*rows*batch floats.     */
+int esgd_rowsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld, int64_t x_sb,
+                    int32_t rows, int64_t cols, int32_t batch, float* scratch, esgd_stream_t stream);
 
 /* max pooling kxk/stride/pad; argmax (flat h*W+w of the input plane, first
  * max in (ky,kx) scan order) kept for backward.                             */

@@ -61,6 +61,12 @@ def nhwc(n, c, h, w) -> Tensor4:
     return Tensor4(n, c, h, w, h * w * c, 1, w * c, c)
 
 
+def cnhw(n, c, h, w, plane_pitch: int) -> Tensor4:
+    """channel-major over the batch: element (img, ci, y, x) at
+    ci*plane_pitch + (img*h + y)*w + x, plane_pitch >= n*h*w."""
+    return Tensor4(n, c, h, w, h * w, plane_pitch, w, 1)
+
+
 _SIGS = {
     "esgd_last_error": (C.c_char_p, []),
     "esgd_abi_version": (C.c_int, []),
@@ -86,8 +92,9 @@ _SIGS = {
     "esgd_softmax_xent_f32": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, i32, i32, i32, vp, vp]),
     "esgd_argmax_rows_f32": (C.c_int, [vp, vp, i64, i32, i32, vp]),
     "esgd_colsum_f32": (C.c_int, [vp, i64, vp, i64, i64, i64, i32, i32, vp, vp]),
-    "esgd_im2col_f32": (C.c_int, [vp, i64, i64, vp, Tensor4, i64, i32, i32, i32, i32, i32, i32, i32, vp]),
-    "esgd_col2im_f32": (C.c_int, [vp, Tensor4, i64, vp, i64, i64, i32, i32, i32, i32, i32, i32, vp, i32, vp]),
+    "esgd_im2col_f32": (C.c_int, [vp, i64, i64, i64, vp, Tensor4, i64, i32, i32, i32, i32, i32, i32, i32, vp]),
+    "esgd_col2im_f32": (C.c_int, [vp, Tensor4, i64, vp, i64, i64, i64, i32, i32, i32, i32, i32, i32, vp, i32, vp]),
+    "esgd_rowsum_f32": (C.c_int, [vp, i64, vp, i64, i64, i32, i64, i32, vp, vp]),
     "esgd_maxpool_fwd_f32": (C.c_int, [vp, Tensor4, i64, vp, vp, Tensor4, i64, i32, i32, i32, i32, vp]),
     "esgd_maxpool_bwd_f32": (C.c_int, [vp, Tensor4, i64, vp, Tensor4, i64, vp, vp, i32, i32, i32, i32, vp]),
     "esgd_copy4_f32": (C.c_int, [vp, Tensor4, i64, vp, Tensor4, i64, i32, vp]),

@@ -17,51 +17,55 @@ __device__ __forceinline__ int64_t off4(const esgd_tensor4& t, int64_t n, int64_
   return n * t.sn + c * t.sc + h * t.sh + w * t.sw;
 }
 
-// one thread per column element; consecutive threads walk a column row
-__global__ void __launch_bounds__(256) k_im2col(float* __restrict__ col, int64_t ldc,
+// im2col, col element (pix, k) at col[pix*col_sp + k*col_sk]. Threads walk
+// the unit-stride side of the destination so stores coalesce: k-fastest for
+// the row layout (col_sk == 1), pixel-fastest for the transposed layout the
+// engine uses (col_sp == 1; reads then also coalesce along ox).
+// 32-bit index math (host checks the sizes).
+template <bool PIX_FAST>
+__global__ void __launch_bounds__(256) k_im2col(float* __restrict__ col, int64_t col_sp, int64_t col_sk,
                                                 int64_t col_sb, const float* __restrict__ x,
                                                 esgd_tensor4 xd, int64_t x_sb, int kh, int kw,
                                                 int stride, int pad, int oh, int ow) {
   const int z = blockIdx.y;
-  const int64_t rows = (int64_t)xd.n * oh * ow;
-  const int64_t total = rows * ldc;
-  const int kdim = xd.c * kh * kw;
+  const int np = xd.n * oh * ow, khw = kh * kw, kdim = xd.c * khw, ohw = oh * ow;
+  const unsigned total = (unsigned)np * (unsigned)kdim;
   const float* xz = x + z * x_sb;
   float* cz = col + z * col_sb;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / ldc;
-    const int k = (int)(e - row * ldc);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    int pix, k;
+    if (PIX_FAST) { k = (int)(e / (unsigned)np); pix = (int)(e - (unsigned)k * np); }
+    else { pix = (int)(e / (unsigned)kdim); k = (int)(e - (unsigned)pix * kdim); }
+    const int img = pix / ohw, p = pix - img * ohw;
+    const int oy = p / ow, ox = p - oy * ow;
+    const int ci = k / khw, r = k - ci * khw;
+    const int ky = r / kw, kx = r - ky * kw;
+    const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
     float v = 0.f;
-    if (k < kdim) {
-      const int img = (int)(row / ((int64_t)oh * ow));
-      const int pix = (int)(row - (int64_t)img * oh * ow);
-      const int oy = pix / ow, ox = pix - oy * ow;
-      const int ci = k / (kh * kw), r = k - ci * kh * kw;
-      const int ky = r / kw, kx = r - ky * kw;
-      const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
-      if (iy >= 0 && iy < xd.h && ix >= 0 && ix < xd.w) v = __ldg(xz + off4(xd, img, ci, iy, ix));
-    }
-    cz[e] = v;
+    if (iy >= 0 && iy < xd.h && ix >= 0 && ix < xd.w)
+      v = __ldg(xz + img * xd.sn + ci * xd.sc + iy * xd.sh + ix * xd.sw);
+    cz[pix * col_sp + k * col_sk] = v;
   }
 }
 
+// col2im (gather form): dx(img, ci, y, x) = sum over (ky, kx) in fixed order
+// of the dcol entries that im2col took from (y, x). Thread order is
+// x-fastest, so both the dcol reads (transposed layout) and the dx writes of
+// the CNHW engine layout coalesce.
 __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_tensor4 xd,
                                                 int64_t x_sb, const float* __restrict__ dcol,
-                                                int64_t ldc, int64_t col_sb, int kh, int kw,
-                                                int stride, int pad, int oh, int ow,
+                                                int64_t col_sp, int64_t col_sk, int64_t col_sb, int kh,
+                                                int kw, int stride, int pad, int oh, int ow,
                                                 const float* __restrict__ mask) {
   const int z = blockIdx.y;
-  const int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
+  const unsigned total = (unsigned)xd.n * xd.c * xd.h * xd.w;
   const float* dz = dcol + z * col_sb;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    // canonical (img, ci, y, x) order of the element
-    int64_t t = e;
-    const int xw = (int)(t % xd.w); t /= xd.w;
-    const int yh = (int)(t % xd.h); t /= xd.h;
-    const int ci = (int)(t % xd.c);
-    const int img = (int)(t / xd.c);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    unsigned t = e;
+    const int xw = (int)(t % (unsigned)xd.w); t /= (unsigned)xd.w;
+    const int yh = (int)(t % (unsigned)xd.h); t /= (unsigned)xd.h;
+    const int img = (int)(t % (unsigned)xd.n);
+    const int ci = (int)(t / (unsigned)xd.n);
     float acc = 0.f;
     for (int ky = 0; ky < kh; ++ky) {
       const int ny = yh + pad - ky;
@@ -73,11 +77,11 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
         if (nx < 0 || nx % stride) continue;
         const int ox = nx / stride;
         if (ox >= ow) continue;
-        const int64_t row = ((int64_t)img * oh + oy) * ow + ox;
-        acc += __ldg(dz + row * ldc + (ci * kh + ky) * kw + kx);
+        const int pix = (img * oh + oy) * ow + ox;
+        acc += __ldg(dz + pix * col_sp + ((ci * kh + ky) * kw + kx) * col_sk);
       }
     }
-    const int64_t o = z * x_sb + off4(xd, img, ci, yh, xw);
+    const int64_t o = z * x_sb + img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
     if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
     dx[o] = acc;
   }
@@ -88,14 +92,13 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(float* __restrict__ y, esgd
                                                      const float* __restrict__ x, esgd_tensor4 xd,
                                                      int64_t x_sb, int k, int stride, int pad) {
   const int z = blockIdx.y;
-  const int64_t total = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = e;
-    const int ox = (int)(t % yd.w); t /= yd.w;
-    const int oy = (int)(t % yd.h); t /= yd.h;
-    const int c = (int)(t % yd.c);
-    const int img = (int)(t / yd.c);
+  const unsigned total = (unsigned)yd.n * yd.c * yd.h * yd.w;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    unsigned t = e;
+    const int ox = (int)(t % (unsigned)yd.w); t /= (unsigned)yd.w;
+    const int oy = (int)(t % (unsigned)yd.h); t /= (unsigned)yd.h;
+    const int c = (int)(t % (unsigned)yd.c);
+    const int img = (int)(t / (unsigned)yd.c);
     float best = -INFINITY;
     int bi = -1;
     for (int ky = 0; ky < k; ++ky) {
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(float* __restrict__ y, esgd
       }
     }
     y[z * y_sb + off4(yd, img, c, oy, ox)] = best;
-    amax[z * total + e] = bi;
+    amax[(int64_t)z * total + e] = bi;
   }
 }
 
@@ -120,15 +123,14 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(float* __restrict__ dx, esg
                                                      const float* __restrict__ mask, int k,
                                                      int stride, int pad) {
   const int z = blockIdx.y;
-  const int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
+  const unsigned total = (unsigned)xd.n * xd.c * xd.h * xd.w;
   const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = e;
-    const int ix = (int)(t % xd.w); t /= xd.w;
-    const int iy = (int)(t % xd.h); t /= xd.h;
-    const int c = (int)(t % xd.c);
-    const int img = (int)(t / xd.c);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    unsigned t = e;
+    const int ix = (int)(t % (unsigned)xd.w); t /= (unsigned)xd.w;
+    const int iy = (int)(t % (unsigned)xd.h); t /= (unsigned)xd.h;
+    const int c = (int)(t % (unsigned)xd.c);
+    const int img = (int)(t / (unsigned)xd.c);
     const int me = iy * xd.w + ix;
     // windows covering iy: oy*stride - pad <= iy <= oy*stride - pad + k - 1
     int oy_lo = iy + pad - k + 1;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(float* __restrict__ dx, esg
     float acc = 0.f;
     for (int oy = oy_lo; oy <= oy_hi; ++oy)
       for (int ox = ox_lo; ox <= ox_hi; ++ox) {
-        const int64_t ye = (((int64_t)img * yd.c + c) * yd.h + oy) * yd.w + ox;
+        const unsigned ye = (((unsigned)img * yd.c + c) * yd.h + oy) * yd.w + ox;
         if (amax[z * ytotal + ye] == me) acc += __ldg(dy + z * y_sb + off4(yd, img, c, oy, ox));
       }
     const int64_t o = z * x_sb + off4(xd, img, c, iy, ix);
@@ -155,19 +157,58 @@ __global__ void __launch_bounds__(256) k_copy4(float* __restrict__ dst, esgd_ten
                                                int64_t d_sb, const float* __restrict__ src,
                                                esgd_tensor4 sd, int64_t s_sb) {
   const int z = blockIdx.y;
-  const int64_t total = (int64_t)dd.n * dd.c * dd.h * dd.w;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = e;
-    const int w = (int)(t % dd.w); t /= dd.w;
-    const int h = (int)(t % dd.h); t /= dd.h;
-    const int c = (int)(t % dd.c);
-    const int n = (int)(t / dd.c);
+  const unsigned total = (unsigned)dd.n * dd.c * dd.h * dd.w;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    unsigned t = e;
+    const int w = (int)(t % (unsigned)dd.w); t /= (unsigned)dd.w;
+    const int h = (int)(t % (unsigned)dd.h); t /= (unsigned)dd.h;
+    const int c = (int)(t % (unsigned)dd.c);
+    const int n = (int)(t / (unsigned)dd.c);
     dst[z * d_sb + off4(dd, n, c, h, w)] = __ldg(src + z * s_sb + off4(sd, n, c, h, w));
   }
 }
 
-bool valid4(const esgd_tensor4& t) { return t.n >= 1 && t.c >= 1 && t.h >= 1 && t.w >= 1; }
+bool valid4(const esgd_tensor4& t) {
+  return t.n >= 1 && t.c >= 1 && t.h >= 1 && t.w >= 1 &&
+         (int64_t)t.n * t.c * t.h * t.w < (int64_t(1) << 31);
+}
+
+// Row sums: out[z*out_sb + r] = sum_{j < cols} x[z*x_sb + r*ld + j] (conv bias
+// gradients over the channel-major activation rows). Pass 1: CTA per (row,
+// chunk), 4 independent partials per thread + fixed-order block tree.
+__global__ void __launch_bounds__(256) k_rowsum_partial(float* part, const float* __restrict__ x, int64_t ld,
+                                                        int64_t x_sb, int cols, int chunk, float* out,
+                                                        int64_t out_sb, int direct) {
+  __shared__ float red[256];
+  const int r = blockIdx.x, ch = blockIdx.y, z = blockIdx.z;
+  const float* row = x + z * x_sb + r * ld;
+  const int j0 = ch * chunk, j1 = min(cols, j0 + chunk);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int j = j0 + threadIdx.x;
+  for (; j + 768 < j1; j += 1024) {
+    s0 += __ldg(row + j); s1 += __ldg(row + j + 256); s2 += __ldg(row + j + 512); s3 += __ldg(row + j + 768);
+  }
+  for (; j < j1; j += 256) s0 += __ldg(row + j);
+  red[threadIdx.x] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (direct) out[z * out_sb + r] = red[0];
+    else part[((int64_t)z * gridDim.x + r) * gridDim.y + ch] = red[0];
+  }
+}
+__global__ void k_rowsum_final(float* out, int64_t out_sb, const float* part, int rows, int nchunk, int batch) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * batch) return;
+  const int z = i / rows, r = i % rows;
+  const float* p = part + ((int64_t)z * rows + r) * nchunk;
+  float t = 0.f;
+  for (int k = 0; k < nchunk; ++k) t += p[k];
+  out[z * out_sb + r] = t;
+}
 
 }  // namespace
 }  // namespace esgd
@@ -175,36 +216,70 @@ bool valid4(const esgd_tensor4& t) { return t.n >= 1 && t.c >= 1 && t.h >= 1 && 
 using namespace esgd;
 #define ESGD_STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
-extern "C" int esgd_im2col_f32(float* col, int64_t ldc, int64_t col_sb, const float* x,
-                               esgd_tensor4 xd, int64_t x_sb, int32_t kh, int32_t kw,
+extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64_t col_sb,
+                               const float* x, esgd_tensor4 xd, int64_t x_sb, int32_t kh, int32_t kw,
                                int32_t stride, int32_t pad, int32_t oh, int32_t ow, int32_t batch,
                                esgd_stream_t stream) {
   ESGD_REQUIRE(valid4(xd) && kh >= 1 && kw >= 1 && stride >= 1 && pad >= 0 && oh >= 1 &&
                    ow >= 1 && batch >= 1,
                ESGD_ERR_SHAPE, "im2col: bad geometry");
-  ESGD_REQUIRE(ldc >= (int64_t)xd.c * kh * kw, ESGD_ERR_SHAPE, "im2col: ldc < C*kh*kw");
+  const int64_t np = (int64_t)xd.n * oh * ow, kdim = (int64_t)xd.c * kh * kw;
+  ESGD_REQUIRE(np * kdim < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED, "im2col: more than 2^31 elements");
+  ESGD_REQUIRE((col_sk == 1 && col_sp >= kdim) || (col_sp == 1 && col_sk >= np), ESGD_ERR_SHAPE,
+               "im2col: col strides must be (>=K, 1) or (1, >=pixels)");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "im2col: batch > 65535");
   ESGD_REQUIRE(col && x, ESGD_ERR_INPUT, "im2col: null buffer");
-  int64_t total = (int64_t)xd.n * oh * ow * ldc;
-  dim3 grid(stride_grid(total, 256, 16), batch);
-  k_im2col<<<grid, 256, 0, ESGD_STREAM(stream)>>>(col, ldc, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
+  dim3 grid(stride_grid(np * kdim, 256, 16), batch);
+  if (col_sp == 1)
+    k_im2col<true><<<grid, 256, 0, ESGD_STREAM(stream)>>>(col, col_sp, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
+  else
+    k_im2col<false><<<grid, 256, 0, ESGD_STREAM(stream)>>>(col, col_sp, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
   return check_launch("esgd_im2col_f32");
 }
 
 extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol,
-                               int64_t ldc, int64_t col_sb, int32_t kh, int32_t kw, int32_t stride,
-                               int32_t pad, int32_t oh, int32_t ow, const float* mask,
+                               int64_t col_sp, int64_t col_sk, int64_t col_sb, int32_t kh, int32_t kw,
+                               int32_t stride, int32_t pad, int32_t oh, int32_t ow, const float* mask,
                                int32_t batch, esgd_stream_t stream) {
   ESGD_REQUIRE(valid4(xd) && kh >= 1 && kw >= 1 && stride >= 1 && pad >= 0 && oh >= 1 &&
                    ow >= 1 && batch >= 1,
                ESGD_ERR_SHAPE, "col2im: bad geometry");
-  ESGD_REQUIRE(ldc >= (int64_t)xd.c * kh * kw, ESGD_ERR_SHAPE, "col2im: ldc < C*kh*kw");
+  const int64_t np = (int64_t)xd.n * oh * ow, kdim = (int64_t)xd.c * kh * kw;
+  ESGD_REQUIRE((col_sk == 1 && col_sp >= kdim) || (col_sp == 1 && col_sk >= np), ESGD_ERR_SHAPE,
+               "col2im: col strides must be (>=K, 1) or (1, >=pixels)");
+  ESGD_REQUIRE(np * kdim < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED, "col2im: more than 2^31 elements");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "col2im: batch > 65535");
   ESGD_REQUIRE(dx && dcol, ESGD_ERR_INPUT, "col2im: null buffer");
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
-  k_col2im<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, ldc, col_sb, kh, kw, stride, pad, oh, ow, mask);
+  k_col2im<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sp, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
   return check_launch("esgd_col2im_f32");
+}
+
+extern "C" int esgd_rowsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld, int64_t x_sb,
+                               int32_t rows, int64_t cols, int32_t batch, float* scratch,
+                               esgd_stream_t stream) {
+  ESGD_REQUIRE(rows >= 1 && cols >= 1 && batch >= 1 && ld >= cols && cols < (int64_t(1) << 31),
+               ESGD_ERR_SHAPE, "rowsum: bad shape");
+  ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "rowsum: null buffer");
+  ESGD_REQUIRE(rows <= 65535 && batch <= 65535, ESGD_ERR_UNSUPPORTED, "rowsum: grid too large");
+  // ~2 CTAs per SM overall, chunks of >= 4096 elements
+  int64_t nchunk = (2 * kNumSMs + (int64_t)rows * batch - 1) / ((int64_t)rows * batch);
+  int64_t maxc = (cols + 4095) / 4096;
+  if (nchunk > maxc) nchunk = maxc;
+  if (nchunk > 64) nchunk = 64;
+  if (nchunk < 1) nchunk = 1;
+  const int64_t chunk = (cols + nchunk - 1) / nchunk;
+  nchunk = (cols + chunk - 1) / chunk;
+  ESGD_REQUIRE(nchunk == 1 || scratch, ESGD_ERR_INPUT, "rowsum: scratch required");
+  cudaStream_t st = ESGD_STREAM(stream);
+  dim3 grid(rows, (unsigned)nchunk, batch);
+  k_rowsum_partial<<<grid, 256, 0, st>>>(scratch, x, ld, x_sb, (int)cols, (int)chunk, out, out_sb, nchunk == 1);
+  if (nchunk > 1) {
+    int tot = rows * batch;
+    k_rowsum_final<<<(tot + 255) / 256, 256, 0, st>>>(out, out_sb, scratch, rows, (int)nchunk, batch);
+  }
+  return check_launch("esgd_rowsum_f32");
 }
 
 extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int32_t* argmax,

@@ -8,8 +8,15 @@ GPU cost the same number of launches as one. Layouts in HBM:
 * parameters / gradients: rows of a (nrep, ldw) fp32 tensor, the reference's
   packed order (network.view_table);
 * sampled batch: (nrep, b, C*H*W) — dataset rows are CHW-flat;
-* conv / pool activations: NHWC per image, (b*OH*OW, C) row-major, so the
-  conv GEMM is  out[b*OH*OW, Cout] = im2col[b*OH*OW, K] . W[Cout, K]^T;
+* conv / pool activations: channel-major over the batch ("CNHW"): channel c
+  is one plane of b*OH*OW pixels (pitch NP4 = b*OH*OW rounded up to 4), so
+  every elementwise / gather kernel walks unit-stride pixels and the GEMMs
+  store coalesced;
+* im2col is transposed, colT[K][NP4]; then
+    forward  out[pix, co]  = colT^T . W^T        (A M-major, B K-major)
+    wgrad    dW[co, kk]    = delta . colT^T      (A K-major, B K-major)
+    dgrad    dcolT[kk,pix] = (delta^T . W)^T     (A M-major, B N-major)
+  and col2im gathers dcolT back to the input planes;
 * dense activations: (b, out); the conv->dense flatten is converted to the
   reference's (c, h, w) order by one strided copy.
 
@@ -27,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import ACT, GemmDesc, TcGemmDesc, Tensor4, nchw, nhwc
+from ._lib import ACT, GemmDesc, TcGemmDesc, Tensor4, cnhw, nchw
 from .device import round_up
 from .errors import InputError, ShapeError
 from .network import Conv, ConvNetSpec, Dense, ModelSpec, Pool, view_table
@@ -50,8 +57,9 @@ class _Layer:
     w_off: int = -1
     b_off: int = -1
     k: int = 0                 # conv reduction dim Cin*k*k
-    kp: int = 0                # padded row pitch of im2col
+    kp: int = 0                # K rounded up to 4 (padded weight pitch)
     flatten_in: bool = False   # dense whose input is a spatial tensor
+    np4: int = 0               # output plane pitch (b*OH*OW rounded up to 4)
 
 
 class DeviceNet:
@@ -115,18 +123,26 @@ class DeviceNet:
         max_act = b * self.d_in
         max_cols = 1
         for L in self.layers:
-            size = b * L.cout * L.hout * L.wout
+            if L.kind in ("conv", "pool"):
+                L.np4 = round_up(b * L.hout * L.wout, 4)
+                size = L.cout * L.np4
+            else:
+                size = b * L.cout
             max_act = max(max_act, size, b * L.cin * L.hin * L.win)
+            if L.flatten_in or L.kind != "dense":
+                prev = self.layers[self.layers.index(L) - 1] if self.layers.index(L) > 0 else None
+                if prev is not None and prev.kind != "dense":
+                    max_act = max(max_act, prev.cout * prev.np4)
             self.outs.append(self._t(size))
-            self.cols.append(self._t(b * L.hout * L.wout * L.kp) if L.kind == "conv" else None)
-            self.amax.append(self._t(size, torch.int32) if L.kind == "pool" else None)
+            self.cols.append(self._t(L.k * L.np4) if L.kind == "conv" else None)
+            self.amax.append(self._t(b * L.cout * L.hout * L.wout, torch.int32) if L.kind == "pool" else None)
             self.flat.append(self._t(b * L.cin * L.hin * L.win) if (L.kind == "dense" and L.flatten_in) else None)
             self.pre.append(self._t(size) if (L.kind == "dense" and L.act in (2, 3)) else None)
             if L.kind in ("conv", "dense"):
                 max_cols = max(max_cols, L.cout)
         self.d_a = self._t(max_act)
         self.d_b = self._t(max_act)
-        self.dcol = self._t(max((b * L.hout * L.wout * L.kp for L in self.layers if L.kind == "conv"), default=4))
+        self.dcol = self._t(max((L.k * L.np4 for L in self.layers if L.kind == "conv"), default=4))
         self.scratch = torch.zeros(256 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
         # split-K partials of the FFMA GEMM (weight gradients reduce over b*OH*OW)
@@ -136,6 +152,12 @@ class DeviceNet:
         # copy each round so the forward GEMM can take them through TMA
         self.wpad = [self._t(L.cout * L.kp) if (L.kind == "conv" and L.k % 4) else None for L in self.layers]
         self.tc_calls = self.ffma_calls = 0
+
+    def _out_desc(self, i: int) -> Tensor4:
+        L = self.layers[i]
+        if L.kind in ("conv", "pool"):
+            return cnhw(self.b, L.cout, L.hout, L.wout, L.np4)
+        return nchw(self.b, L.cout, 1, 1)
 
     # ---- GEMM routing ------------------------------------------------------
     def _gemm(self, stream, m, n, k, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
@@ -177,14 +199,14 @@ class DeviceNet:
         xin = self.x if x is None else x
         cur, cur_sb = xin.data_ptr(), xin.stride(0)
         cur_d = nchw(b, self.c0, self.h0, self.w0)
-        cur_flat = True   # current tensor is (b, features) row-major
         for i, L in enumerate(self.layers):
             out = self.outs[i]
             o, o_sb = out.data_ptr(), out.stride(0)
             if L.kind == "conv":
                 col = self.cols[i]
                 lay = L.lay
-                _lib.check(lib.esgd_im2col_f32(col.data_ptr(), L.kp, col.stride(0), cur, cur_d, cur_sb,
+                npix = b * L.hout * L.wout
+                _lib.check(lib.esgd_im2col_f32(col.data_ptr(), 1, L.np4, col.stride(0), cur, cur_d, cur_sb,
                                                lay.k, lay.k, lay.stride, lay.pad, L.hout, L.wout, nb,
                                                stream), "im2col")
                 w_ptr, w_pitch, w_sb = wp + 4 * L.w_off, L.k, ldw
@@ -194,18 +216,16 @@ class DeviceNet:
                                                   pw.stride(0), w_ptr, Tensor4(1, L.cout, 1, L.k, 0, L.k, 0, 1),
                                                   ldw, nb, stream), "pad_weights")
                     w_ptr, w_pitch, w_sb = pw.data_ptr(), L.kp, pw.stride(0)
-                self._gemm(stream, b * L.hout * L.wout, L.cout, L.k,
-                           col.data_ptr(), L.kp, 1, col.stride(0),
+                # out[pix, co] = sum_k colT[k, pix] W[co, k] + b[co]  (CNHW store)
+                self._gemm(stream, npix, L.cout, L.k,
+                           col.data_ptr(), 1, L.np4, col.stride(0),
                            w_ptr, 1, w_pitch, w_sb,
-                           o, L.cout, 1, o_sb, bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act)
-                cur_d = nhwc(b, L.cout, L.hout, L.wout)
-                cur_flat = False
+                           o, 1, L.np4, o_sb, bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act)
             elif L.kind == "pool":
                 lay = L.lay
-                yd = nhwc(b, L.cout, L.hout, L.wout)
-                _lib.check(lib.esgd_maxpool_fwd_f32(o, yd, o_sb, self.amax[i].data_ptr(), cur, cur_d, cur_sb,
-                                                    lay.k, lay.stride, lay.pad, nb, stream), "maxpool")
-                cur_d = yd
+                _lib.check(lib.esgd_maxpool_fwd_f32(o, self._out_desc(i), o_sb, self.amax[i].data_ptr(), cur,
+                                                    cur_d, cur_sb, lay.k, lay.stride, lay.pad, nb, stream),
+                           "maxpool")
             else:
                 if L.flatten_in:
                     f = self.flat[i]
@@ -218,9 +238,8 @@ class DeviceNet:
                            wp + 4 * L.w_off, L.cout, 1, ldw, o, L.cout, 1, o_sb,
                            bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act,
                            pre=None if pre is None else pre.data_ptr())
-                cur_d = nchw(b, L.cout, 1, 1)
-                cur_flat = True
             cur, cur_sb = o, o_sb
+            cur_d = self._out_desc(i)
         return self.outs[-1]
 
     def _input_of(self, i: int):
@@ -230,9 +249,8 @@ class DeviceNet:
             return (self.x.data_ptr(), self.x.stride(0), nchw(b, self.c0, self.h0, self.w0), 0)
         P = self.layers[i - 1]
         t = self.outs[i - 1]
-        d = nhwc(b, P.cout, P.hout, P.wout) if P.kind in ("conv", "pool") else nchw(b, P.cout, 1, 1)
         act = P.act if P.kind != "pool" else 0
-        return (t.data_ptr(), t.stride(0), d, act)
+        return (t.data_ptr(), t.stride(0), self._out_desc(i - 1), act)
 
     def _other(self, t: torch.Tensor) -> torch.Tensor:
         return self.d_b if t is self.d_a else self.d_a
@@ -292,37 +310,37 @@ class DeviceNet:
                                                   nchw(b, L.cin, L.hin, L.win), dnext.stride(0), nb, stream),
                                "unflatten")
                     if pact == 1:
-                        self._act_bwd(dback, xin, x_sb, b * fan_in, 1, stream)
+                        self._act_bwd(dback, xin, x_sb, xd.c * xd.sc, 1, stream)
                     dnext = dback
                 dcur = dnext
             elif L.kind == "pool":
                 lay = L.lay
-                yd = nhwc(b, L.cout, L.hout, L.wout)
+                yd = self._out_desc(i)
                 dnext = self._other(dcur)
                 mask = xin if pact == 1 else None
                 _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd, d_sb,
                                                     self.amax[i].data_ptr(), mask, lay.k, lay.stride, lay.pad,
                                                     nb, stream), "maxpool_bwd")
                 dcur = dnext
-            else:  # conv
+            else:  # conv: delta is CNHW [Cout][np4]
                 lay = L.lay
                 col = self.cols[i]
-                pix = b * L.hout * L.wout
-                # dW[Cout, K] = delta^T . col
-                self._gemm(stream, L.cout, L.k, pix, dcur.data_ptr(), 1, L.cout, d_sb,
-                           col.data_ptr(), L.kp, 1, col.stride(0),
+                npix = b * L.hout * L.wout
+                # dW[co, kk] = sum_pix delta[co, pix] colT[kk, pix]
+                self._gemm(stream, L.cout, L.k, npix, dcur.data_ptr(), L.np4, 1, d_sb,
+                           col.data_ptr(), 1, L.np4, col.stride(0),
                            gp + 4 * L.w_off, L.k, 1, ldg)
-                _lib.check(lib.esgd_colsum_f32(gp + 4 * L.b_off, ldg, dcur.data_ptr(), L.cout, d_sb, pix, L.cout,
-                                               nb, self.scratch.data_ptr(), stream), "colsum")
+                _lib.check(lib.esgd_rowsum_f32(gp + 4 * L.b_off, ldg, dcur.data_ptr(), L.np4, d_sb, L.cout, npix,
+                                               nb, self.scratch.data_ptr(), stream), "rowsum")
                 if not need_dx:
                     continue
-                # dcol[pix, K] = delta . W ; dx = col2im(dcol) (relu-masked by the producer)
-                self._gemm(stream, pix, L.k, L.cout, dcur.data_ptr(), L.cout, 1, d_sb,
+                # dcolT[kk, pix] = sum_co W[co, kk] delta[co, pix]; dx = col2im(dcolT)
+                self._gemm(stream, npix, L.k, L.cout, dcur.data_ptr(), 1, L.np4, d_sb,
                            wp + 4 * L.w_off, L.k, 1, ldw,
-                           self.dcol.data_ptr(), L.kp, 1, self.dcol.stride(0))
+                           self.dcol.data_ptr(), 1, L.np4, self.dcol.stride(0))
                 dnext = self._other(dcur)
                 mask = xin if pact == 1 else None
-                _lib.check(lib.esgd_col2im_f32(dnext.data_ptr(), xd, dnext.stride(0), self.dcol.data_ptr(), L.kp,
-                                               self.dcol.stride(0), lay.k, lay.k, lay.stride, lay.pad,
+                _lib.check(lib.esgd_col2im_f32(dnext.data_ptr(), xd, dnext.stride(0), self.dcol.data_ptr(), 1,
+                                               L.np4, self.dcol.stride(0), lay.k, lay.k, lay.stride, lay.pad,
                                                L.hout, L.wout, mask, nb, stream), "col2im")
                 dcur = dnext

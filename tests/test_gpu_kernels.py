@@ -202,14 +202,14 @@ def test_im2col_col2im_adjoint_and_oracle():
     kp = (K + 3) // 4 * 4
     col = torch.zeros((n * oh * ow, kp), device="cuda")
     xd = dev(x)
-    _lib.call("esgd_im2col_f32", col.data_ptr(), kp, 0, xd.data_ptr(), _lib.nchw(n, c, h, w), 0,
+    _lib.call("esgd_im2col_f32", col.data_ptr(), kp, 1, 0, xd.data_ptr(), _lib.nchw(n, c, h, w), 0,
               k, k, s, p, oh, ow, 1, stream_ptr())
     ref, _, _ = O._im2col(x, k, s, p)
     assert np.array_equal(host(col)[:, :K], ref)
     dcol = rng.standard_normal((n * oh * ow, kp)).astype(np.float32)
     dx = torch.zeros((n, c, h, w), device="cuda")
     dcd = dev(dcol)
-    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dcd.data_ptr(), kp, 0,
+    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dcd.data_ptr(), kp, 1, 0,
               k, k, s, p, oh, ow, None, 1, stream_ptr())
     exp = O._col2im(dcol[:, :K].copy(), (n, c, h, w), k, s, p, oh, ow)
     assert np.array_equal(host(dx), exp)
@@ -266,3 +266,38 @@ def test_tcgen05_gemm_mn_major_and_split_k(a_major, b_major, m, n, k, batch):
     d.c = C2.data_ptr()
     _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
     assert torch.equal(Cd, C2)
+
+
+def test_transposed_im2col_cnhw_and_rowsum():
+    """the engine's layouts: CNHW input planes, transposed colT[K][pixels]."""
+    rng = np.random.default_rng(5)
+    n, c, h, w, k, s, p = 3, 4, 9, 10, 3, 2, 1
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    npix = n * oh * ow
+    np4 = (npix + 3) // 4 * 4
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    plane = (n * h * w + 3) // 4 * 4
+    xc = np.zeros((c, plane), np.float32)
+    xc[:, :n * h * w] = x.transpose(1, 0, 2, 3).reshape(c, -1)
+    K = c * k * k
+    colT = torch.zeros((K, np4), device="cuda")
+    xcd = dev(xc)
+    _lib.call("esgd_im2col_f32", colT.data_ptr(), 1, np4, 0, xcd.data_ptr(), _lib.cnhw(n, c, h, w, plane), 0,
+              k, k, s, p, oh, ow, 1, stream_ptr())
+    ref, _, _ = O._im2col(x, k, s, p)
+    assert np.array_equal(host(colT)[:, :npix].T, ref)
+    dcolT = np.zeros((K, np4), np.float32)
+    dcolT[:, :npix] = rng.standard_normal((K, npix))
+    dd = dev(dcolT)
+    dx = torch.zeros((c, plane), device="cuda")
+    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.cnhw(n, c, h, w, plane), 0, dd.data_ptr(), 1, np4, 0,
+              k, k, s, p, oh, ow, None, 1, stream_ptr())
+    exp = O._col2im(dcolT[:, :npix].T.copy(), (n, c, h, w), k, s, p, oh, ow)
+    assert np.array_equal(host(dx)[:, :n * h * w].reshape(c, n, h, w).transpose(1, 0, 2, 3), exp)
+    rows = rng.standard_normal((7, 50000)).astype(np.float32)
+    out = torch.zeros(7, device="cuda")
+    scratch = torch.zeros(64 * 7, device="cuda")
+    rd = dev(rows)
+    _lib.call("esgd_rowsum_f32", out.data_ptr(), 0, rd.data_ptr(), 50000, 0, 7, 50000, 1, scratch.data_ptr(),
+              stream_ptr())
+    assert rel_err(host(out), rows.astype(np.float64).sum(axis=1)) < 1e-5
