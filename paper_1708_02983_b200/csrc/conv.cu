@@ -87,6 +87,120 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
   }
 }
 
+// ---- division-free variants used by the engine (CTA per (channel-or-k,
+// image, replica), 32x8 threads over the output plane) ------------------------
+
+// transposed im2col: colT[k][pix]; the CTA owns one k = (ci, ky, kx) of one
+// image, so reads walk ix with the conv stride and writes walk pixels.
+__global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
+                                                  const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
+                                                  int kh, int kw, int stride, int pad, int oh, int ow) {
+  const int k = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
+  const int khw = kh * kw, ci = k / khw, r = k - ci * khw, ky = r / kw, kx = r - ky * kw;
+  const float* xp = x + z * x_sb + img * xd.sn + ci * xd.sc;
+  float* cp = col + z * col_sb + k * col_sk + (int64_t)img * oh * ow;
+  for (int oy = threadIdx.y; oy < oh; oy += blockDim.y) {
+    const int iy = oy * stride - pad + ky;
+    const bool vy = iy >= 0 && iy < xd.h;
+    for (int ox = threadIdx.x; ox < ow; ox += blockDim.x) {
+      const int ix = ox * stride - pad + kx;
+      cp[oy * ow + ox] = (vy && ix >= 0 && ix < xd.w) ? __ldg(xp + iy * xd.sh + ix * xd.sw) : 0.f;
+    }
+  }
+}
+
+// col2im from colT, CTA per (ci, image): dx plane of one channel, (ky, kx)
+// accumulation order fixed; STRIDE1 removes the divisibility tests.
+template <bool STRIDE1>
+__global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+                                                  const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
+                                                  int kh, int kw, int stride, int pad, int oh, int ow,
+                                                  const float* __restrict__ mask) {
+  const int ci = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
+  const float* dz = dcol + z * col_sb + (int64_t)(ci * kh * kw) * col_sk + (int64_t)img * oh * ow;
+  const int64_t base = z * x_sb + img * xd.sn + ci * xd.sc;
+  for (int yh = threadIdx.y; yh < xd.h; yh += blockDim.y) {
+    for (int xw = threadIdx.x; xw < xd.w; xw += blockDim.x) {
+      float acc = 0.f;
+      for (int ky = 0; ky < kh; ++ky) {
+        int oy = yh + pad - ky;
+        if (oy < 0) continue;
+        if (!STRIDE1) { if (oy % stride) continue; oy /= stride; }
+        if (oy >= oh) continue;
+        for (int kx = 0; kx < kw; ++kx) {
+          int ox = xw + pad - kx;
+          if (ox < 0) continue;
+          if (!STRIDE1) { if (ox % stride) continue; ox /= stride; }
+          if (ox >= ow) continue;
+          acc += __ldg(dz + (int64_t)(ky * kw + kx) * col_sk + oy * ow + ox);
+        }
+      }
+      const int64_t o = base + yh * xd.sh + xw * xd.sw;
+      if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
+      dx[o] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
+                                                       int32_t* __restrict__ amax, const float* __restrict__ x,
+                                                       esgd_tensor4 xd, int64_t x_sb, int k, int stride, int pad) {
+  const int c = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
+  const float* xp = x + z * x_sb + img * xd.sn + c * xd.sc;
+  const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
+  int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * yd.h * yd.w;
+  float* yp = y + z * y_sb + img * yd.sn + c * yd.sc;
+  for (int oy = threadIdx.y; oy < yd.h; oy += blockDim.y) {
+    for (int ox = threadIdx.x; ox < yd.w; ox += blockDim.x) {
+      float best = -INFINITY;
+      int bi = -1;
+      for (int ky = 0; ky < k; ++ky) {
+        const int iy = oy * stride - pad + ky;
+        if (iy < 0 || iy >= xd.h) continue;
+        for (int kx = 0; kx < k; ++kx) {
+          const int ix = ox * stride - pad + kx;
+          if (ix < 0 || ix >= xd.w) continue;
+          const float v = __ldg(xp + iy * xd.sh + ix * xd.sw);
+          if (bi < 0 || v > best) { best = v; bi = iy * xd.w + ix; }
+        }
+      }
+      yp[oy * yd.sh + ox * yd.sw] = best;
+      ap[oy * yd.w + ox] = bi;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+                                                       const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
+                                                       const int32_t* __restrict__ amax,
+                                                       const float* __restrict__ mask, int k, int stride, int pad) {
+  const int c = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
+  const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
+  const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * yd.h * yd.w;
+  const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
+  const int64_t base = z * x_sb + img * xd.sn + c * xd.sc;
+  for (int iy = threadIdx.y; iy < xd.h; iy += blockDim.y) {
+    int oy_lo = iy + pad - k + 1;
+    oy_lo = oy_lo <= 0 ? 0 : (oy_lo + stride - 1) / stride;
+    int oy_hi = (iy + pad) / stride;
+    if (oy_hi > yd.h - 1) oy_hi = yd.h - 1;
+    for (int ix = threadIdx.x; ix < xd.w; ix += blockDim.x) {
+      const int me = iy * xd.w + ix;
+      int ox_lo = ix + pad - k + 1;
+      ox_lo = ox_lo <= 0 ? 0 : (ox_lo + stride - 1) / stride;
+      int ox_hi = (ix + pad) / stride;
+      if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
+      float acc = 0.f;
+      for (int oy = oy_lo; oy <= oy_hi; ++oy)
+        for (int ox = ox_lo; ox <= ox_hi; ++ox)
+          if (ap[oy * yd.w + ox] == me) acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
+      const int64_t o = base + iy * xd.sh + ix * xd.sw;
+      if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
+      dx[o] = acc;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_maxpool_fwd(float* __restrict__ y, esgd_tensor4 yd,
                                                      int64_t y_sb, int32_t* __restrict__ amax,
                                                      const float* __restrict__ x, esgd_tensor4 xd,
@@ -229,6 +343,11 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
                "im2col: col strides must be (>=K, 1) or (1, >=pixels)");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "im2col: batch > 65535");
   ESGD_REQUIRE(col && x, ESGD_ERR_INPUT, "im2col: null buffer");
+  if (col_sp == 1 && xd.n <= 65535) {
+    dim3 g2((unsigned)kdim, xd.n, batch), b2(32, 8);
+    k_im2col_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
+    return check_launch("esgd_im2col_f32");
+  }
   dim3 grid(stride_grid(np * kdim, 256, 16), batch);
   if (col_sp == 1)
     k_im2col<true><<<grid, 256, 0, ESGD_STREAM(stream)>>>(col, col_sp, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
@@ -250,6 +369,14 @@ extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const f
   ESGD_REQUIRE(np * kdim < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED, "col2im: more than 2^31 elements");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "col2im: batch > 65535");
   ESGD_REQUIRE(dx && dcol, ESGD_ERR_INPUT, "col2im: null buffer");
+  if (col_sp == 1 && xd.n <= 65535) {
+    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+    if (stride == 1)
+      k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
+    else
+      k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
+    return check_launch("esgd_col2im_f32");
+  }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
   k_col2im<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sp, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
@@ -291,6 +418,11 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
                ESGD_ERR_SHAPE, "maxpool_fwd: bad geometry");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(y && argmax && x, ESGD_ERR_INPUT, "maxpool_fwd: null buffer");
+  if (xd.n <= 65535) {
+    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+    k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad);
+    return check_launch("esgd_maxpool_fwd_f32");
+  }
   int64_t total = (int64_t)yd.n * yd.c * yd.h * yd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
   k_maxpool_fwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad);
@@ -306,6 +438,11 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
                ESGD_ERR_SHAPE, "maxpool_bwd: bad geometry");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(dx && dy && argmax, ESGD_ERR_INPUT, "maxpool_bwd: null buffer");
+  if (xd.n <= 65535) {
+    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, k, stride, pad);
+    return check_launch("esgd_maxpool_bwd_f32");
+  }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
   k_maxpool_bwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, k, stride, pad);

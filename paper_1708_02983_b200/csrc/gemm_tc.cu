@@ -170,7 +170,7 @@ struct Epi {
   const float* mask; int64_t mask_sm, mask_sn, mask_sb;
   int act, accumulate, m, n, k;
   float* ws;        // split-K partials [batch][splits][m][n]
-  int splits, kb_per_split;
+  int splits, kb_per_split, batch;
 };
 
 __device__ __forceinline__ float epi_apply(const Epi& ep, float x, int z, int row, int col, int64_t off,
@@ -222,6 +222,29 @@ __device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, int bytes,
   }
 }
 
+// Work unit = (n tile, m tile, batch z, K slice); units are dealt to the
+// persistent CTAs round-robin. Every role walks the same unit sequence, so the
+// smem-stage ring (global k-block counter) and the TMEM-accumulator ring
+// (global chunk counter) stay in lockstep across units: the TMA of unit u+1
+// overlaps the MMAs of unit u, and the epilogue of unit u overlaps both.
+struct Unit {
+  int n0, m0, z, slice, kb0, nkb;
+};
+__device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, int nkb_all, int BN_) {
+  Unit w;
+  const int per_z = ntn * ntm * ep.splits;
+  w.z = u / per_z;
+  int r = u - w.z * per_z;
+  w.slice = r / (ntn * ntm);
+  r -= w.slice * ntn * ntm;
+  // n fastest: consecutive CTAs share the A (M) tile in L2
+  w.m0 = (r / ntn) * BM;
+  w.n0 = (r % ntn) * BN_;
+  w.kb0 = w.slice * ep.kb_per_split;
+  w.nkb = max(0, min(nkb_all - w.kb0, ep.kb_per_split));
+  return w;
+}
+
 template <int BN, bool SPLIT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -237,12 +260,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                  aempty0 = afull0 + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int z = blockIdx.z / ep.splits, slice = blockIdx.z % ep.splits;
+  const int ntn = (ep.n + BN - 1) / BN, ntm = (ep.m + BM - 1) / BM;
   const int nkb_all = (ep.k + BK - 1) / BK;
-  const int kb0 = slice * ep.kb_per_split;
-  const int nkb = max(0, min(nkb_all - kb0, ep.kb_per_split));  // k-blocks of this slice
-  const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
+  const int nunits = ntn * ntm * ep.splits * ep.batch;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -270,64 +290,76 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::kStages;
-        if (kb >= C::kStages) mbar_wait(empty0 + 8 * s, ((kb / C::kStages) - 1) & 1);
-        uint8_t* st = smem + s * C::kStageBytes;
-        mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
-        load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, kb0 + kb, m0, z);
-        load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, kb0 + kb, n0, z);
+      uint32_t g = 0;  // global k-block counter (stage ring position)
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % C::kStages;
+          if (g >= (uint32_t)C::kStages) mbar_wait(empty0 + 8 * s, ((g / C::kStages) - 1) & 1);
+          uint8_t* st = smem + s * C::kStageBytes;
+          mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
+          load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
+          load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb, w.n0, w.z);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
       constexpr uint32_t idesc = idesc_tf32(BM, BN, AMN, BMN);
-      for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c >= 2) mbar_wait(aempty0 + 8 * buf, ((c >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t acc = tmem + buf * BN;
-        const int kb_end = min(nkb, (c + 1) * kChunkKB);
-        for (int kb = c * kChunkKB; kb < kb_end; ++kb) {
-          const int s = kb % C::kStages;
-          const uint32_t ph = (kb / C::kStages) & 1;
-          if (SPLIT) mbar_wait(split0 + 8 * s, ph);
-          else mbar_wait(full0 + 8 * s, ph);
+      uint32_t g = 0, c = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+        for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
+          const int buf = c & 1;
+          if (c >= 2) mbar_wait(aempty0 + 8 * buf, ((c >> 1) - 1) & 1);
           tc_fence_after();
-          const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+          const uint32_t acc = tmem + buf * BN;
+          const int kend = min(w.nkb, kc + kChunkKB);
+          for (int kb = kc; kb < kend; ++kb, ++g) {
+            const int s = g % C::kStages;
+            const uint32_t ph = (g / C::kStages) & 1;
+            if (SPLIT) mbar_wait(split0 + 8 * s, ph);
+            else mbar_wait(full0 + 8 * s, ph);
+            tc_fence_after();
+            const uint32_t st = smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            // K-major: 8 tf32 = 32 B along K inside the swizzle atom;
-            // MN-major: one 8-row K-atom (1024 B) per instruction
-            const uint64_t ah = op_desc<AMN>(st, kk), bh = op_desc<BMN>(st + C::kOffB, kk);
-            const uint32_t acc0 = (kb > c * kChunkKB || kk > 0) ? 1u : 0u;
-            if (SPLIT) {
-              const uint64_t al = op_desc<AMN>(st + C::kOffALo, kk),
-                             bl = op_desc<BMN>(st + C::kOffBLo, kk);
-              mma_tf32(acc, al, bh, idesc, acc0);  // small terms first
-              mma_tf32(acc, ah, bl, idesc, 1u);
-              mma_tf32(acc, ah, bh, idesc, 1u);
-            } else {
-              mma_tf32(acc, ah, bh, idesc, acc0);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              // K-major: 8 tf32 = 32 B along K inside the swizzle atom;
+              // MN-major: one 8-row K slab (1024 B) per instruction
+              const uint64_t ah = op_desc<AMN>(st, kk), bh = op_desc<BMN>(st + C::kOffB, kk);
+              const uint32_t acc0 = (kb > kc || kk > 0) ? 1u : 0u;
+              if (SPLIT) {
+                const uint64_t al = op_desc<AMN>(st + C::kOffALo, kk),
+                               bl = op_desc<BMN>(st + C::kOffBLo, kk);
+                mma_tf32(acc, al, bh, idesc, acc0);  // small terms first
+                mma_tf32(acc, ah, bl, idesc, 1u);
+                mma_tf32(acc, ah, bh, idesc, 1u);
+              } else {
+                mma_tf32(acc, ah, bh, idesc, acc0);
+              }
             }
+            mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
           }
-          mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
+          mma_commit(afull0 + 8 * buf);  // this chunk's partial sum is complete
         }
-        mma_commit(afull0 + 8 * buf);  // this chunk's partial sum is complete
       }
     }
   } else if (warp < 6) {
     if (SPLIT) {  // ---- split warps: raw tile -> (hi in place, lo twin)
       const int et = threadIdx.x - 64;  // 0..127
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::kStages;
-        mbar_wait(full0 + 8 * s, (kb / C::kStages) & 1);
-        uint8_t* st = smem + s * C::kStageBytes;
-        split_tile(st, st + C::kOffALo, kTileBytesA, et);
-        split_tile(st + C::kOffB, st + C::kOffBLo, C::kTileBytesB, et);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(split0 + 8 * s);
+      uint32_t g = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+        for (int kb = 0; kb < w.nkb; ++kb, ++g) {
+          const int s = g % C::kStages;
+          mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
+          uint8_t* st = smem + s * C::kStageBytes;
+          split_tile(st, st + C::kOffALo, kTileBytesA, et);
+          split_tile(st + C::kOffB, st + C::kOffBLo, C::kTileBytesB, et);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(split0 + 8 * s);
+        }
       }
     }
   } else {
@@ -336,39 +368,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     // round-to-nearest adds (promotion): the tensor-core accumulator only ever
     // sums kChunkKB*32 products, which keeps the long-K error fp32-grade.
     const int q = warp & 3;
-    float racc[BN];
+    uint32_t c = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+      float racc[BN];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) racc[j] = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
-      tc_fence_after();
+      for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+      for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
+        const int buf = c & 1;
+        mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c0, v);
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
+          for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
-    }
-    const int row = m0 + q * 32 + lane;
-    if (row < ep.m) {
-      if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
-        float* P = ep.ws + ((int64_t)z * ep.splits + slice) * ep.m * ep.n + (int64_t)row * ep.n;
+      const int row = w.m0 + q * 32 + lane;
+      if (row < ep.m) {
+        if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
+          float* P = ep.ws + ((int64_t)w.z * ep.splits + w.slice) * ep.m * ep.n + (int64_t)row * ep.n;
 #pragma unroll
-        for (int j = 0; j < BN; ++j)
-          if (n0 + j < ep.n) P[n0 + j] = racc[j];
-      } else {
-        float* cz = ep.c + z * ep.c_sb;
+          for (int j = 0; j < BN; ++j)
+            if (w.n0 + j < ep.n) P[w.n0 + j] = racc[j];
+        } else {
+          float* cz = ep.c + w.z * ep.c_sb;
 #pragma unroll
-        for (int j = 0; j < BN; ++j) {
-          const int col = n0 + j;
-          if (col < ep.n) {
-            const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
-            cz[off] = epi_apply(ep, racc[j], z, row, col, off, cz);
+          for (int j = 0; j < BN; ++j) {
+            const int col = w.n0 + j;
+            if (col < ep.n) {
+              const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+              cz[off] = epi_apply(ep, racc[j], w.z, row, col, off, cz);
+            }
           }
         }
       }
@@ -464,8 +500,10 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   kbps = (kbps + kChunkKB - 1) / kChunkKB * kChunkKB;
   splits = (nkb + kbps - 1) / kbps;
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
-         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps};
-  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch * splits);
+         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch};
+  // persistent: one CTA per SM (smem-limited), units dealt round-robin
+  const int64_t units = (int64_t)tiles * splits;
+  const int grid = (int)std::min<int64_t>(units, kNumSMs);
   k_tc_gemm<BN, SPLIT, AMN, BMN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, ep);
   if (splits > 1) {
     dim3 rg(stride_grid((int64_t)d->m * d->n, 256, 8), d->batch);
@@ -499,8 +537,8 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
   ESGD_REQUIRE(aligned16(d->a) && aligned16(d->b), ESGD_ERR_INPUT, "tc_gemm: A/B must be 16-B aligned");
   ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
                "tc_gemm: batch strides must be multiples of 4");
-  ESGD_REQUIRE(d->batch <= 65535 && (d->m + tc::BM - 1) / tc::BM <= 65535, ESGD_ERR_UNSUPPORTED,
-               "tc_gemm: grid too large");
+  ESGD_REQUIRE((int64_t)((d->m + tc::BM - 1) / tc::BM) * ((d->n + 63) / 64) * d->batch < (int64_t(1) << 30),
+               ESGD_ERR_UNSUPPORTED, "tc_gemm: too many tiles");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool split = d->precision == 3;
   if (d->n <= 64) return split ? tc::launch_major<64, true>(d, st) : tc::launch_major<64, false>(d, st);
