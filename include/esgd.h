@@ -189,6 +189,11 @@ int esgd_softmax_xent_f32(float* dlogits, float* row_loss, const float* logits, 
                           int32_t rows, int32_t cols, int32_t batch, int32_t* bad_label,
                           esgd_stream_t stream);
 
+/* batched transpose: dst[z][c*ldd + r] = src[z][r*lds + c], r < rows, c < cols
+ * (operand re-layout so no tensor-core GEMM needs two MN-major operands).   */
+int esgd_transpose_f32(float* dst, int64_t ldd, int64_t d_sb, const float* src, int64_t lds,
+                       int64_t s_sb, int32_t rows, int32_t cols, int32_t batch, esgd_stream_t stream);
+
 /* argmax per row (ties -> lowest index), records.py:92-101 */
 int esgd_argmax_rows_f32(int32_t* out, const float* x, int64_t ld, int32_t rows, int32_t cols,
                          esgd_stream_t stream);

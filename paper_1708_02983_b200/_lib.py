@@ -90,6 +90,7 @@ _SIGS = {
     "esgd_act_fwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),
     "esgd_act_bwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),
     "esgd_softmax_xent_f32": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, i32, i32, i32, vp, vp]),
+    "esgd_transpose_f32": (C.c_int, [vp, i64, i64, vp, i64, i64, i32, i32, i32, vp]),
     "esgd_argmax_rows_f32": (C.c_int, [vp, vp, i64, i32, i32, vp]),
     "esgd_colsum_f32": (C.c_int, [vp, i64, vp, i64, i64, i64, i32, i32, vp, vp]),
     "esgd_im2col_f32": (C.c_int, [vp, i64, i64, i64, vp, Tensor4, i64, i32, i32, i32, i32, i32, i32, i32, vp]),

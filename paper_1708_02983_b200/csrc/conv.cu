@@ -87,86 +87,98 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
   }
 }
 
-// ---- division-free variants used by the engine (CTA per (channel-or-k,
-// image, replica), 32x8 threads over the output plane) ------------------------
+// ---- engine variants: thread <-> pixel of the whole batch (b*OH*OW), the
+// pixel decomposition is done once and reused over a group of 16 k / channel
+// values taken from blockIdx.y, so the inner loop is address math + one
+// coalesced load and store (no per-element divisions) -------------------------
+constexpr int kGroup = 16;
 
-// transposed im2col: colT[k][pix]; the CTA owns one k = (ci, ky, kx) of one
-// image, so reads walk ix with the conv stride and writes walk pixels.
+// transposed im2col colT[k][pix]
 __global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
                                                   const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
                                                   int kh, int kw, int stride, int pad, int oh, int ow) {
-  const int k = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
-  const int khw = kh * kw, ci = k / khw, r = k - ci * khw, ky = r / kw, kx = r - ky * kw;
-  const float* xp = x + z * x_sb + img * xd.sn + ci * xd.sc;
-  float* cp = col + z * col_sb + k * col_sk + (int64_t)img * oh * ow;
-  for (int oy = threadIdx.y; oy < oh; oy += blockDim.y) {
-    const int iy = oy * stride - pad + ky;
-    const bool vy = iy >= 0 && iy < xd.h;
-    for (int ox = threadIdx.x; ox < ow; ox += blockDim.x) {
-      const int ix = ox * stride - pad + kx;
-      cp[oy * ow + ox] = (vy && ix >= 0 && ix < xd.w) ? __ldg(xp + iy * xd.sh + ix * xd.sw) : 0.f;
-    }
+  const int z = blockIdx.z;
+  const int np = xd.n * oh * ow, kdim = xd.c * kh * kw, khw = kh * kw;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= np) return;
+  const int ohw = oh * ow, img = pix / ohw, p = pix - img * ohw, oy = p / ow, ox = p - oy * ow;
+  const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
+  const float* xz = x + z * x_sb + img * xd.sn;
+  float* cz = col + z * col_sb + pix;
+  const int k0 = blockIdx.y * kGroup, k1 = min(kdim, k0 + kGroup);
+  int ci = k0 / khw, r = k0 - ci * khw, ky = r / kw, kx = r - ky * kw;
+  for (int k = k0; k < k1; ++k) {
+    const int iy = iy0 + ky, ix = ix0 + kx;
+    float v = 0.f;
+    if (iy >= 0 && iy < xd.h && ix >= 0 && ix < xd.w) v = __ldg(xz + ci * xd.sc + iy * xd.sh + ix * xd.sw);
+    cz[k * col_sk] = v;
+    if (++kx == kw) { kx = 0; if (++ky == kh) { ky = 0; ++ci; } }
   }
 }
 
-// col2im from colT, CTA per (ci, image): dx plane of one channel, (ky, kx)
-// accumulation order fixed; STRIDE1 removes the divisibility tests.
+// col2im from colT: thread <-> input pixel (img, y, x), channels of a group;
+// (ky, kx) accumulation order fixed per element.
 template <bool STRIDE1>
 __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                   const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                   int kh, int kw, int stride, int pad, int oh, int ow,
                                                   const float* __restrict__ mask) {
-  const int ci = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
-  const float* dz = dcol + z * col_sb + (int64_t)(ci * kh * kw) * col_sk + (int64_t)img * oh * ow;
-  const int64_t base = z * x_sb + img * xd.sn + ci * xd.sc;
-  for (int yh = threadIdx.y; yh < xd.h; yh += blockDim.y) {
-    for (int xw = threadIdx.x; xw < xd.w; xw += blockDim.x) {
-      float acc = 0.f;
-      for (int ky = 0; ky < kh; ++ky) {
-        int oy = yh + pad - ky;
-        if (oy < 0) continue;
-        if (!STRIDE1) { if (oy % stride) continue; oy /= stride; }
-        if (oy >= oh) continue;
-        for (int kx = 0; kx < kw; ++kx) {
-          int ox = xw + pad - kx;
-          if (ox < 0) continue;
-          if (!STRIDE1) { if (ox % stride) continue; ox /= stride; }
-          if (ox >= ow) continue;
-          acc += __ldg(dz + (int64_t)(ky * kw + kx) * col_sk + oy * ow + ox);
-        }
+  const int z = blockIdx.z;
+  const int hw = xd.h * xd.w, npin = xd.n * hw;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npin) return;
+  const int img = q / hw, p = q - img * hw, yh = p / xd.w, xw = p - yh * xd.w;
+  const float* dz = dcol + z * col_sb + (int64_t)img * oh * ow;
+  const int c0 = blockIdx.y * kGroup, c1 = min(xd.c, c0 + kGroup);
+  for (int ci = c0; ci < c1; ++ci) {
+    const float* dc = dz + (int64_t)(ci * kh * kw) * col_sk;
+    float acc = 0.f;
+    for (int ky = 0; ky < kh; ++ky) {
+      int oy = yh + pad - ky;
+      if (oy < 0) continue;
+      if (!STRIDE1) { if (oy % stride) continue; oy /= stride; }
+      if (oy >= oh) continue;
+      for (int kx = 0; kx < kw; ++kx) {
+        int ox = xw + pad - kx;
+        if (ox < 0) continue;
+        if (!STRIDE1) { if (ox % stride) continue; ox /= stride; }
+        if (ox >= ow) continue;
+        acc += __ldg(dc + (int64_t)(ky * kw + kx) * col_sk + oy * ow + ox);
       }
-      const int64_t o = base + yh * xd.sh + xw * xd.sw;
-      if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-      dx[o] = acc;
     }
+    const int64_t o = z * x_sb + img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
+    dx[o] = acc;
   }
 }
 
+// max pooling, thread <-> output pixel of the batch, channels of a group
 __global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
                                                        int32_t* __restrict__ amax, const float* __restrict__ x,
                                                        esgd_tensor4 xd, int64_t x_sb, int k, int stride, int pad) {
-  const int c = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
-  const float* xp = x + z * x_sb + img * xd.sn + c * xd.sc;
-  const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * yd.h * yd.w;
-  float* yp = y + z * y_sb + img * yd.sn + c * yd.sc;
-  for (int oy = threadIdx.y; oy < yd.h; oy += blockDim.y) {
-    for (int ox = threadIdx.x; ox < yd.w; ox += blockDim.x) {
-      float best = -INFINITY;
-      int bi = -1;
-      for (int ky = 0; ky < k; ++ky) {
-        const int iy = oy * stride - pad + ky;
-        if (iy < 0 || iy >= xd.h) continue;
-        for (int kx = 0; kx < k; ++kx) {
-          const int ix = ox * stride - pad + kx;
-          if (ix < 0 || ix >= xd.w) continue;
-          const float v = __ldg(xp + iy * xd.sh + ix * xd.sw);
-          if (bi < 0 || v > best) { best = v; bi = iy * xd.w + ix; }
-        }
+  const int z = blockIdx.z;
+  const int ohw = yd.h * yd.w, np = yd.n * ohw;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= np) return;
+  const int img = q / ohw, p = q - img * ohw, oy = p / yd.w, ox = p - oy * yd.w;
+  const int64_t ytotal = (int64_t)yd.n * yd.c * ohw;
+  const int c0 = blockIdx.y * kGroup, c1 = min(yd.c, c0 + kGroup);
+  for (int c = c0; c < c1; ++c) {
+    const float* xp = x + z * x_sb + img * xd.sn + c * xd.sc;
+    float best = -INFINITY;
+    int bi = -1;
+    for (int ky = 0; ky < k; ++ky) {
+      const int iy = oy * stride - pad + ky;
+      if (iy < 0 || iy >= xd.h) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int ix = ox * stride - pad + kx;
+        if (ix < 0 || ix >= xd.w) continue;
+        const float v = __ldg(xp + iy * xd.sh + ix * xd.sw);
+        if (bi < 0 || v > best) { best = v; bi = iy * xd.w + ix; }
       }
-      yp[oy * yd.sh + ox * yd.sw] = best;
-      ap[oy * yd.w + ox] = bi;
     }
+    y[z * y_sb + img * yd.sn + c * yd.sc + oy * yd.sh + ox * yd.sw] = best;
+    amax[z * ytotal + ((int64_t)img * yd.c + c) * ohw + p] = bi;
   }
 }
 
@@ -174,30 +186,31 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                        const int32_t* __restrict__ amax,
                                                        const float* __restrict__ mask, int k, int stride, int pad) {
-  const int c = blockIdx.x, img = blockIdx.y, z = blockIdx.z;
-  const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * yd.h * yd.w;
-  const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
-  const int64_t base = z * x_sb + img * xd.sn + c * xd.sc;
-  for (int iy = threadIdx.y; iy < xd.h; iy += blockDim.y) {
-    int oy_lo = iy + pad - k + 1;
-    oy_lo = oy_lo <= 0 ? 0 : (oy_lo + stride - 1) / stride;
-    int oy_hi = (iy + pad) / stride;
-    if (oy_hi > yd.h - 1) oy_hi = yd.h - 1;
-    for (int ix = threadIdx.x; ix < xd.w; ix += blockDim.x) {
-      const int me = iy * xd.w + ix;
-      int ox_lo = ix + pad - k + 1;
-      ox_lo = ox_lo <= 0 ? 0 : (ox_lo + stride - 1) / stride;
-      int ox_hi = (ix + pad) / stride;
-      if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
-      float acc = 0.f;
-      for (int oy = oy_lo; oy <= oy_hi; ++oy)
-        for (int ox = ox_lo; ox <= ox_hi; ++ox)
-          if (ap[oy * yd.w + ox] == me) acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
-      const int64_t o = base + iy * xd.sh + ix * xd.sw;
-      if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-      dx[o] = acc;
-    }
+  const int z = blockIdx.z;
+  const int hw = xd.h * xd.w, npin = xd.n * hw, ohw = yd.h * yd.w;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npin) return;
+  const int img = q / hw, p = q - img * hw, iy = p / xd.w, ix = p - iy * xd.w;
+  const int64_t ytotal = (int64_t)yd.n * yd.c * ohw;
+  int oy_lo = iy + pad - k + 1;
+  oy_lo = oy_lo <= 0 ? 0 : (oy_lo + stride - 1) / stride;
+  int oy_hi = (iy + pad) / stride;
+  if (oy_hi > yd.h - 1) oy_hi = yd.h - 1;
+  int ox_lo = ix + pad - k + 1;
+  ox_lo = ox_lo <= 0 ? 0 : (ox_lo + stride - 1) / stride;
+  int ox_hi = (ix + pad) / stride;
+  if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
+  const int c0 = blockIdx.y * kGroup, c1 = min(xd.c, c0 + kGroup);
+  for (int c = c0; c < c1; ++c) {
+    const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
+    const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
+    float acc = 0.f;
+    for (int oy = oy_lo; oy <= oy_hi; ++oy)
+      for (int ox = ox_lo; ox <= ox_hi; ++ox)
+        if (ap[oy * yd.w + ox] == p) acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
+    const int64_t o = z * x_sb + img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
+    dx[o] = acc;
   }
 }
 
@@ -343,9 +356,9 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
                "im2col: col strides must be (>=K, 1) or (1, >=pixels)");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "im2col: batch > 65535");
   ESGD_REQUIRE(col && x, ESGD_ERR_INPUT, "im2col: null buffer");
-  if (col_sp == 1 && xd.n <= 65535) {
-    dim3 g2((unsigned)kdim, xd.n, batch), b2(32, 8);
-    k_im2col_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
+  if (col_sp == 1 && (kdim + kGroup - 1) / kGroup <= 65535) {
+    dim3 g2((unsigned)((np + 255) / 256), (unsigned)((kdim + kGroup - 1) / kGroup), batch);
+    k_im2col_t<<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
     return check_launch("esgd_im2col_f32");
   }
   dim3 grid(stride_grid(np * kdim, 256, 16), batch);
@@ -369,8 +382,9 @@ extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const f
   ESGD_REQUIRE(np * kdim < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED, "col2im: more than 2^31 elements");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "col2im: batch > 65535");
   ESGD_REQUIRE(dx && dcol, ESGD_ERR_INPUT, "col2im: null buffer");
-  if (col_sp == 1 && xd.n <= 65535) {
-    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+  if (col_sp == 1) {
+    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
+    dim3 b2(256);
     if (stride == 1)
       k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
     else
@@ -418,8 +432,9 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
                ESGD_ERR_SHAPE, "maxpool_fwd: bad geometry");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(y && argmax && x, ESGD_ERR_INPUT, "maxpool_fwd: null buffer");
-  if (xd.n <= 65535) {
-    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+  {
+    dim3 g2((unsigned)(((int64_t)yd.n * yd.h * yd.w + 255) / 256), (unsigned)((yd.c + kGroup - 1) / kGroup), batch);
+    dim3 b2(256);
     k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad);
     return check_launch("esgd_maxpool_fwd_f32");
   }
@@ -438,8 +453,9 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
                ESGD_ERR_SHAPE, "maxpool_bwd: bad geometry");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(dx && dy && argmax, ESGD_ERR_INPUT, "maxpool_bwd: null buffer");
-  if (xd.n <= 65535) {
-    dim3 g2(xd.c, xd.n, batch), b2(32, 8);
+  {
+    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
+    dim3 b2(256);
     k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, k, stride, pad);
     return check_launch("esgd_maxpool_bwd_f32");
   }

@@ -293,6 +293,28 @@ __global__ void k_colsum_final(float* out, int64_t out_sb, const float* part, in
   out[z * out_sb + c] = t0 + t1;
 }
 
+// batched 2-D transpose through a padded 32x33 smem tile (both sides coalesced)
+__global__ void __launch_bounds__(256) k_transpose(float* __restrict__ dst, int64_t ldd, int64_t d_sb,
+                                                   const float* __restrict__ src, int64_t lds, int64_t s_sb,
+                                                   int rows, int cols) {
+  __shared__ float tile[32][33];
+  const int z = blockIdx.z;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const float* sz = src + z * s_sb;
+  float* dz = dst + z * d_sb;
+#pragma unroll
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? __ldg(sz + (int64_t)r * lds + c) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dz[(int64_t)c * ldd + r] = tile[threadIdx.x][i];
+  }
+}
+
 }  // namespace
 }  // namespace esgd
 
@@ -393,4 +415,17 @@ extern "C" int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64
     k_colsum_final<<<(tot + 255) / 256, 256, 0, st>>>(out, out_sb, scratch, (int)nchunk, cols, batch);
   }
   return check_launch("esgd_colsum_f32");
+}
+
+extern "C" int esgd_transpose_f32(float* dst, int64_t ldd, int64_t d_sb, const float* src, int64_t lds,
+                                  int64_t s_sb, int32_t rows, int32_t cols, int32_t batch,
+                                  esgd_stream_t stream) {
+  ESGD_REQUIRE(rows >= 0 && cols >= 0 && batch >= 1 && lds >= cols && ldd >= rows, ESGD_ERR_SHAPE,
+               "transpose: bad shape");
+  if (rows == 0 || cols == 0) return ESGD_OK;
+  ESGD_REQUIRE(dst && src, ESGD_ERR_INPUT, "transpose: null buffer");
+  ESGD_REQUIRE((rows + 31) / 32 <= 65535 && batch <= 65535, ESGD_ERR_UNSUPPORTED, "transpose: grid too large");
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batch), block(32, 8);
+  k_transpose<<<grid, block, 0, ESGD_STREAM(stream)>>>(dst, ldd, d_sb, src, lds, s_sb, rows, cols);
+  return check_launch("esgd_transpose_f32");
 }

@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <string.h>
 
 namespace esgd {
 namespace tc {
@@ -49,7 +50,8 @@ struct Cfg {
   static constexpr int kOffALo = kTileBytesA;
   static constexpr int kOffB = SPLIT ? 2 * kTileBytesA : kTileBytesA;
   static constexpr int kOffBLo = kOffB + kTileBytesB;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -171,7 +173,17 @@ struct Epi {
   int act, accumulate, m, n, k;
   float* ws;        // split-K partials [batch][splits][m][n]
   int splits, kb_per_split, batch;
+  int out_mode;     // 0 direct stores, 1 TMA store M-contiguous C, 2 TMA store N-contiguous C
 };
+
+// epilogue value without the read-modify-write of accumulate (TMA-store path)
+__device__ __forceinline__ float epi_value(const Epi& ep, float x, int z, int row, int col) {
+  if (ep.bias && col < ep.n) x = __fadd_rn(x, ep.bias[z * ep.bias_sb + col]);
+  x = act_apply(x, ep.act);
+  if (ep.mask && row < ep.m && col < ep.n)
+    x = __fmul_rn(x, ep.mask[z * ep.mask_sb + (int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
+  return x;
+}
 
 __device__ __forceinline__ float epi_apply(const Epi& ep, float x, int z, int row, int col, int64_t off,
                                            const float* cz) {
@@ -202,23 +214,40 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t tile, int kk) {
   return MN ? desc_sw128_mn(tile + kk * 1024) : desc_sw128(tile + kk * 32);
 }
 
-// split one landed tile: hi = tf32-truncated x (in place), lo = x - hi
-__device__ __forceinline__ void split_tile(uint8_t* raw, uint8_t* lo, int bytes, int tid) {
-  float4* r4 = reinterpret_cast<float4*>(raw);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-  const int n4 = bytes / 16;
-  for (int i = tid; i < n4; i += 128) {
-    float4 x = r4[i], h, l;
-    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-    l.x = __fsub_rn(x.x, h.x);
-    l.y = __fsub_rn(x.y, h.y);
-    l.z = __fsub_rn(x.z, h.z);
-    l.w = __fsub_rn(x.w, h.w);
-    r4[i] = h;
-    l4[i] = l;
+// split one landed tile: hi = tf32-truncated x (in place), lo = x - hi.
+// Shared-window addresses with explicit ld/st.shared.v4 (a generic pointer
+// here costs an address-space check and L1TEX latency per access), eight
+// 16-B loads in flight per thread before any store.
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+template <int BYTES>
+__device__ __forceinline__ void split_tile(uint32_t raw, uint32_t lo, int tid) {
+  constexpr int kVec = BYTES / 16, kPer = kVec / 128, kBatch = kPer < 8 ? kPer : 8;
+  static_assert(kVec % 128 == 0 && kPer % kBatch == 0, "tile must split evenly over 128 threads");
+#pragma unroll
+  for (int b0 = 0; b0 < kPer; b0 += kBatch) {
+    float4 x[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) x[j] = lds4(raw + 16 * (tid + 128 * (b0 + j)));
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const uint32_t off = 16 * (tid + 128 * (b0 + j));
+      float4 h, l;
+      h.x = tf32_hi(x[j].x); h.y = tf32_hi(x[j].y); h.z = tf32_hi(x[j].z); h.w = tf32_hi(x[j].w);
+      l.x = __fsub_rn(x[j].x, h.x); l.y = __fsub_rn(x[j].y, h.y);
+      l.z = __fsub_rn(x[j].z, h.z); l.w = __fsub_rn(x[j].w, h.w);
+      sts4(raw + off, h);
+      sts4(lo + off, l);
+    }
   }
 }
 
@@ -248,11 +277,12 @@ __device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, 
 template <int BN, bool SPLIT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-              Epi ep) {
+              const __grid_constant__ CUtensorMap map_c, Epi ep) {
   using C = Cfg<BN, SPLIT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 32 KB, 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + C::kStageOutBytes);
   // bars: full[S], split[S], empty[S], acc_full[2], acc_empty[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 4);
   const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
@@ -353,9 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
-          uint8_t* st = smem + s * C::kStageBytes;
-          split_tile(st, st + C::kOffALo, kTileBytesA, et);
-          split_tile(st + C::kOffB, st + C::kOffBLo, C::kTileBytesB, et);
+          const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+          split_tile<kTileBytesA>(st, st + C::kOffALo, et);
+          split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(split0 + 8 * s);
@@ -390,25 +420,82 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
       }
       const int row = w.m0 + q * 32 + lane;
-      if (row < ep.m) {
-        if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
+      if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
+        if (row < ep.m) {
           float* P = ep.ws + ((int64_t)w.z * ep.splits + w.slice) * ep.m * ep.n + (int64_t)row * ep.n;
 #pragma unroll
           for (int j = 0; j < BN; ++j)
             if (w.n0 + j < ep.n) P[w.n0 + j] = racc[j];
-        } else {
-          float* cz = ep.c + w.z * ep.c_sb;
+        }
+      } else if (ep.out_mode != 0) {
+        // smem-staged TMA store, 64 columns at a time
+        const uint32_t so = smem_u32(stage_out);
+        float* cz = ep.c + w.z * ep.c_sb;
 #pragma unroll
-          for (int j = 0; j < BN; ++j) {
-            const int col = w.n0 + j;
-            if (col < ep.n) {
-              const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
-              cz[off] = epi_apply(ep, racc[j], w.z, row, col, off, cz);
+        for (int h = 0; h < BN / 64; ++h) {
+          // staging buffer free? (previous bulk store has read it)
+          if (threadIdx.x == 192) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int jj = 0; jj < 64; jj += 4) {
+            float4 v;
+            const int j = h * 64 + jj;
+            v.x = epi_value(ep, racc[j], w.z, row, w.n0 + j);
+            v.y = epi_value(ep, racc[j + 1], w.z, row, w.n0 + j + 1);
+            v.z = epi_value(ep, racc[j + 2], w.z, row, w.n0 + j + 2);
+            v.w = epi_value(ep, racc[j + 3], w.z, row, w.n0 + j + 3);
+            const int r = q * 32 + lane;
+            if (ep.out_mode == 1) {
+              // M-contiguous output: staging [64 cols][128 rows], lanes walk rows
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 0) * 128 + r) * 4), "f"(v.x) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 1) * 128 + r) * 4), "f"(v.y) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 2) * 128 + r) * 4), "f"(v.z) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 3) * 128 + r) * 4), "f"(v.w) : "memory");
+            } else {
+              // N-contiguous output: two 32-col boxes, 128-B rows, 128B swizzle
+              const int box = jj >> 5, chunk = (jj & 31) >> 2;
+              sts4(so + box * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4), v);
             }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 192) {
+            const int ncol = w.n0 + h * 64;
+            if (ep.out_mode == 1) {
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                      reinterpret_cast<uint64_t>(&map_c)),
+                  "r"(w.m0), "r"(ncol), "r"(w.z), "r"(so)
+                  : "memory");
+            } else {
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                      reinterpret_cast<uint64_t>(&map_c)),
+                  "r"(ncol), "r"(w.m0), "r"(w.z), "r"(so)
+                  : "memory");
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                      reinterpret_cast<uint64_t>(&map_c)),
+                  "r"(ncol + 32), "r"(w.m0), "r"(w.z), "r"(so + 16384)
+                  : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          (void)cz;
+        }
+      } else if (row < ep.m) {
+        float* cz = ep.c + w.z * ep.c_sb;
+#pragma unroll
+        for (int j = 0; j < BN; ++j) {
+          const int col = w.n0 + j;
+          if (col < ep.n) {
+            const int64_t off = (int64_t)row * ep.c_sm + (int64_t)col * ep.c_sn;
+            cz[off] = epi_apply(ep, racc[j], w.z, row, col, off, cz);
           }
         }
       }
     }
+    if (ep.out_mode != 0 && threadIdx.x == 192) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -499,12 +586,36 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   int kbps = (nkb + splits - 1) / splits;
   kbps = (kbps + kChunkKB - 1) / kChunkKB * kChunkKB;
   splits = (nkb + kbps - 1) / kbps;
+  // output: TMA store when one C stride is unit and the other 16-B aligned
+  int out_mode = 0;
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof(mc));
+  if (splits == 1 && !d->accumulate && aligned16(d->c) && (d->batch == 1 || (d->c_sb & 3) == 0)) {
+    if (d->c_sm == 1 && (d->c_sn & 3) == 0 && d->c_sn >= d->m) out_mode = 1;
+    else if (d->c_sn == 1 && (d->c_sm & 3) == 0 && d->c_sm >= d->n) out_mode = 2;
+  }
+  if (out_mode) {
+    auto enc = get_encode();
+    const bool mcont = out_mode == 1;
+    const int64_t inner = mcont ? d->m : d->n, outer = mcont ? d->n : d->m;
+    const int64_t ld = mcont ? d->c_sn : d->c_sm;
+    int64_t bstride = d->batch > 1 ? d->c_sb : ld * outer;
+    bstride = (bstride + 3) & ~int64_t(3);
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)d->batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
+    cuuint32_t box[3] = {mcont ? 128u : 32u, mcont ? 64u : 128u, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->c, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, mcont ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) out_mode = 0;
+  }
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
-         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch};
+         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch, out_mode};
   // persistent: one CTA per SM (smem-limited), units dealt round-robin
   const int64_t units = (int64_t)tiles * splits;
   const int grid = (int)std::min<int64_t>(units, kNumSMs);
-  k_tc_gemm<BN, SPLIT, AMN, BMN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, ep);
+  k_tc_gemm<BN, SPLIT, AMN, BMN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, ep);
   if (splits > 1) {
     dim3 rg(stride_grid((int64_t)d->m * d->n, 256, 8), d->batch);
     k_tc_reduce<<<rg, 256, 0, st>>>(ep);

@@ -301,3 +301,31 @@ def test_transposed_im2col_cnhw_and_rowsum():
     _lib.call("esgd_rowsum_f32", out.data_ptr(), 0, rd.data_ptr(), 50000, 0, 7, 50000, 1, scratch.data_ptr(),
               stream_ptr())
     assert rel_err(host(out), rows.astype(np.float64).sum(axis=1)) < 1e-5
+
+
+@pytest.mark.parametrize("m,n,k,c_mcontig", [(300, 70, 96, 1), (1000, 200, 64, 1), (257, 130, 40, 0),
+                                              (128, 64, 32, 1)])
+def test_tcgen05_gemm_tma_store_epilogue(m, n, k, c_mcontig):
+    """TMA-store epilogue for both output orientations (M-contiguous conv /
+    dcolT outputs, N-contiguous weight gradients), with bias + relu + edges."""
+    rng = np.random.default_rng(m + 3 * n + k)
+    kp = (k + 3) // 4 * 4
+    A = np.zeros((m, kp), np.float32)
+    B = np.zeros((n, kp), np.float32)
+    A[:, :k] = rng.standard_normal((m, k))
+    B[:, :k] = rng.standard_normal((n, k))
+    bias = rng.standard_normal(n).astype(np.float32)
+    mp, np_ = (m + 3) // 4 * 4, (n + 3) // 4 * 4
+    c_sm, c_sn = (1, mp) if c_mcontig else (np_, 1)
+    Cd = torch.full((mp * np_,), -5.0, device="cuda")
+    Ad, Bd, bd = dev(A), dev(B), dev(bias)
+    d = _lib.TcGemmDesc(m, n, k, 1, Ad.data_ptr(), kp, 0, Bd.data_ptr(), kp, 0, Cd.data_ptr(), c_sm, c_sn, 0,
+                        bd.data_ptr(), 0, None, 0, 0, 0, 1, 0, 3, 0, 0, None, 0)
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    out = host(Cd)
+    got = np.array([[out[i * c_sm + j * c_sn] for j in range(n)] for i in range(m)])
+    ref = np.maximum(_gemm_ref(A[:, :k], B[:, :k].T) + bias, 0)
+    assert rel_err(got, ref) < 3e-6
+    # padding outside the m x n window untouched
+    if c_mcontig and mp > m:
+        assert out[m] == -5.0

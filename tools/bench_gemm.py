@@ -15,22 +15,23 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1708_02983_b200 import _lib  # noqa: E402
 from paper_1708_02983_b200.device import stream_ptr  # noqa: E402
 
-# (name, m, n, k, a_major, b_major) of AlexNet b=128 in the CNHW engine layout
+# (name, m, n, k, a_major, b_major, c_mcontig) of AlexNet b=128 as the CNHW
+# engine issues them (nets.py): conv outputs / dcolT are M-contiguous
 SHAPES = [
-    ("conv1.fwd", 387200, 64, 363, 1, 0),
-    ("conv2.fwd", 93312, 192, 1600, 1, 0),
-    ("conv3.fwd", 21632, 384, 1728, 1, 0),
-    ("conv2.wgrad", 192, 1600, 93312, 0, 0),
-    ("conv1.wgrad", 64, 363, 387200, 0, 0),
-    ("conv2.dgrad", 93312, 1600, 192, 1, 1),
-    ("conv4.dgrad", 21632, 3456, 256, 1, 1),
-    ("fc6.fwd", 128, 4096, 9216, 0, 1),
-    ("fc6.wgrad", 9216, 4096, 128, 1, 1),
-    ("fc6.dgrad", 128, 9216, 4096, 0, 0),
+    ("conv1.fwd", 387200, 64, 363, 1, 0, 1),
+    ("conv2.fwd", 93312, 192, 1600, 1, 0, 1),
+    ("conv3.fwd", 21632, 384, 1728, 1, 0, 1),
+    ("conv2.wgrad", 192, 1600, 93312, 0, 0, 0),
+    ("conv1.wgrad", 64, 363, 387200, 0, 0, 0),
+    ("conv2.dgrad", 93312, 1600, 192, 1, 0, 1),
+    ("conv4.dgrad", 21632, 3456, 256, 1, 0, 1),
+    ("fc6.fwd", 128, 4096, 9216, 0, 1, 0),
+    ("fc6.wgrad", 9216, 4096, 128, 1, 0, 0),
+    ("fc6.dgrad", 128, 9216, 4096, 0, 0, 0),
 ]
 
 
-def run(name, m, n, k, am, bm, precision, reps=10):
+def run(name, m, n, k, am, bm, cm, precision, reps=10):
     kp = (k + 3) // 4 * 4
     mp = (m + 3) // 4 * 4
     np_ = (n + 3) // 4 * 4
@@ -40,7 +41,9 @@ def run(name, m, n, k, am, bm, precision, reps=10):
     ws = torch.empty(1 << 24, device="cuda")
     lda = mp if am else kp
     ldb = np_ if bm else kp
-    d = _lib.TcGemmDesc(m, n, k, 1, A.data_ptr(), lda, 0, B.data_ptr(), ldb, 0, Cm.data_ptr(), n, 1, 0,
+    c_sm, c_sn = (1, mp) if cm else (np_, 1)
+    Cm = torch.empty((mp * np_,), device="cuda")
+    d = _lib.TcGemmDesc(m, n, k, 1, A.data_ptr(), lda, 0, B.data_ptr(), ldb, 0, Cm.data_ptr(), c_sm, c_sn, 0,
                         None, 0, None, 0, 0, 0, 0, 0, precision, am, bm, ws.data_ptr(), ws.numel())
     lib = _lib.load()
     for _ in range(3):

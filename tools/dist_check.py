@@ -1,0 +1,49 @@
+"""Multi-GPU Sync-EASGD check under torchrun: the run with P workers over N
+ranks (one NCCL allreduce per round, CUDA-graph captured) must equal the
+single-process run bitwise for N = 2 (a two-term sum is order-free) and
+within 1e-6 relative otherwise.
+
+    torchrun --nproc-per-node N tools/dist_check.py
+"""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_1708_02983_b200 import HyperParams, make_config, network, run_trainer  # noqa: E402
+from paper_1708_02983_b200.datasets import gen_synthetic, normalize  # noqa: E402
+from paper_1708_02983_b200.trainers import NetworkProblem  # noqa: E402
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank = dist.get_world_size(), dist.get_rank()
+    train = normalize(gen_synthetic(10, 784, 200, seed=0, separation=5.0))
+    prob = NetworkProblem(network.lenet(seed=0), train)
+    P = 2 * world
+    cfg = make_config("sync-easgd3", workers=P, iterations=12, batch_size=32,
+                      hyper=HyperParams(eta=0.05, rho=0.25), eval_every=6, seed=3)
+    rec = run_trainer(cfg, prob)
+    if rank == 0:
+        dist.destroy_process_group()
+        # the same run in one process (all P workers on this GPU)
+        ref = run_trainer(cfg, prob)
+        err = float(np.linalg.norm(rec.final_weights - ref.final_weights) / np.linalg.norm(ref.final_weights))
+        werr = max(float(np.linalg.norm(a - b) / np.linalg.norm(b))
+                   for a, b in zip(rec.final_worker_weights, ref.final_worker_weights))
+        print(f"world={world} P={P} center rel err {err:.3e} worker max rel err {werr:.3e} "
+              f"bitwise={rec.weights_digest == ref.weights_digest} graph={rec.engine_info.get('graph')}")
+        ok = err < 1e-6 and werr < 1e-6
+        print("DIST_CHECK", "PASS" if ok else "FAIL")
+        sys.exit(0 if ok else 1)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
