@@ -141,6 +141,42 @@ def time_update_kernel(eng, reps: int = 20):
     return bytes_, float(np.mean(times))
 
 
+def time_dominant_gemm(eng, reps: int = 10):
+    """Record one eager gradient pass, re-launch its largest tcgen05 GEMM
+    alone with CUDA events (warm). Returns (desc-summary, flops, seconds)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1708_02983_b200 import _lib
+    from paper_1708_02983_b200.device import stream_ptr
+
+    net = eng.plan.net
+    net.record = []
+    eng.plan.gradient(eng.G.clone(), eng.W.clone(), stream_ptr())
+    torch.cuda.synchronize()
+    recs, net.record = net.record, None
+    tcs = [r for r in recs if r[0] == "tc"]
+    if not tcs:
+        return None
+    lib = _lib.load()
+    best = None
+    for kind, d, flops in tcs:
+        for _ in range(2):
+            _lib.check(lib.esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            _lib.check(lib.esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+        b.record()
+        b.synchronize()
+        t = a.elapsed_time(b) / reps / 1e3
+        if best is None or t > best[2]:
+            best = (f"m={d.m} n={d.n} k={d.k} batch={d.batch} a_major={d.a_major} b_major={d.b_major}",
+                    flops, t, d.precision)
+    return best
+
+
 def run_device(args):
     import torch
     import torch.distributed as dist
@@ -188,11 +224,28 @@ def run_device(args):
     upd_bytes, upd_s = time_update_kernel(eng)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    roof = {"kernel": "esgd_sync_update_f32 (k_sync_update<4>)", "bound": "hbm",
-            "achieved": round(upd_bytes / upd_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": None,
-            "algorithmic_bytes": upd_bytes, "launch_s": upd_s,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"}
+    src = "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback (B200_PROFILING.md)"
+    roof_upd = {"kernel": "esgd_sync_update_f32 (k_sync_update<4>)", "bound": "hbm",
+                "achieved": round(upd_bytes / upd_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": upd_bytes, "launch_s": upd_s,
+                "peak_source": f"{src} hbm_gbs (copy)"}
+    # dominant kernel of the step: the largest tcgen05 3xTF32 GEMM launch,
+    # re-launched alone (warm) with CUDA events; tf32-pipe rate = 3 x 2MNK / t
+    # against the measured bf16 peak / 2 (nominal dense tf32 = bf16 / 2)
+    dom = time_dominant_gemm(eng)
+    if dom is not None:
+        desc, fl, t, prec = dom
+        tf32_peak = pk.get("bf16_tflops", 1590.0) / 2
+        ach = prec * fl / t / 1e12
+        roof = {"kernel": f"esgd_tc_gemm_f32 (k_tc_gemm, {desc})", "bound": "tensor",
+                "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                "frac": round(ach / tf32_peak, 4), "traffic": None,
+                "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
+                "algorithmic_flops_per_launch": fl,
+                "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)"}
+    else:
+        roof = roof_upd
 
     # e2e: run_trainer's host data path (pinned batch H2D + loss D2H every round)
     e2e = run_e2e(args, spec, train, cfg, world) if not args.no_e2e else None
@@ -211,6 +264,7 @@ def run_device(args):
                    "l2": "update kernel timed with L2 flushed; step inputs resident",
                    "graph": eng.graph is not None},
         "roofline": roof,
+        "roofline_update": roof_upd,
         "comm_fraction_exposed": round(comm_frac, 4),
         "gpu_launches": launches_per_step(eng) * args.steps,
         "e2e": e2e,
@@ -220,8 +274,13 @@ def run_device(args):
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
+        # captured graphs hold NCCL work; tearing the communicator down under
+        # them can hang, so release them, sync, and leave without a teardown
+        eng.graph = None
+        torch.cuda.synchronize()
         dist.barrier()
-        dist.destroy_process_group()
+        sys.stdout.flush()
+        os._exit(0)
 
 
 def launches_per_step(eng) -> int:

@@ -227,11 +227,12 @@ int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64_t col_sb, 
 
 /* col2im (adjoint of im2col, gather form, fixed (ky, kx) order): dx(img,ci,y,x)
  * = sum of the dcol entries im2col took from (y,x); optional mask multiplies
- * the result by (mask>0) with mask laid out like dx (relu-grad).           */
+ * the result by (mask>0); mask has dx's layout within a batch entry and its
+ * own batch stride mask_sb (relu-grad from the producer's activation).     */
 int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol, int64_t col_sp,
                     int64_t col_sk, int64_t col_sb, int32_t kh, int32_t kw, int32_t stride,
-                    int32_t pad, int32_t oh, int32_t ow, const float* mask, int32_t batch,
-                    esgd_stream_t stream);
+                    int32_t pad, int32_t oh, int32_t ow, const float* mask, int64_t mask_sb,
+                    int32_t batch, esgd_stream_t stream);
 
 /* row sums: out[z*out_sb + r] = sum_{j<cols} x[z*x_sb + r*ld + j] (conv bias
  * gradients over channel-major activations; network.py:195 generalised).
@@ -244,11 +245,12 @@ int esgd_rowsum_f32(float* out, int64_t out_sb, const float* x, int64_t ld, int6
 int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int32_t* argmax,
                          const float* x, esgd_tensor4 xd, int64_t x_sb, int32_t k,
                          int32_t stride, int32_t pad, int32_t batch, esgd_stream_t stream);
-/* dx = sum of dy routed to argmax (gather form), optional relu mask (x>0). */
+/* dx = sum of dy routed to argmax (gather form), optional relu mask (x>0)
+ * with dx's layout and batch stride mask_sb.                                */
 int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
                          esgd_tensor4 yd, int64_t y_sb, const int32_t* argmax,
-                         const float* mask, int32_t k, int32_t stride, int32_t pad,
-                         int32_t batch, esgd_stream_t stream);
+                         const float* mask, int64_t mask_sb, int32_t k, int32_t stride,
+                         int32_t pad, int32_t batch, esgd_stream_t stream);
 
 /* strided 4-D copy (layout change, e.g. NHWC -> NCHW flatten for the FC
  * head and back), optional relu mask on the source (src>0 of mask).         */

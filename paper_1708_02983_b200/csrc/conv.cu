@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
                                                 int64_t x_sb, const float* __restrict__ dcol,
                                                 int64_t col_sp, int64_t col_sk, int64_t col_sb, int kh,
                                                 int kw, int stride, int pad, int oh, int ow,
-                                                const float* __restrict__ mask) {
+                                                const float* __restrict__ mask, int64_t mask_sb) {
   const int z = blockIdx.y;
   const unsigned total = (unsigned)xd.n * xd.c * xd.h * xd.w;
   const float* dz = dcol + z * col_sb;
@@ -81,9 +81,9 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
         acc += __ldg(dz + pix * col_sp + ((ci * kh + ky) * kw + kx) * col_sk);
       }
     }
-    const int64_t o = z * x_sb + img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
-    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-    dx[o] = acc;
+    const int64_t o = img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    dx[z * x_sb + o] = acc;
   }
 }
 
@@ -122,7 +122,7 @@ template <bool STRIDE1>
 __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                   const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                   int kh, int kw, int stride, int pad, int oh, int ow,
-                                                  const float* __restrict__ mask) {
+                                                  const float* __restrict__ mask, int64_t mask_sb) {
   const int z = blockIdx.z;
   const int hw = xd.h * xd.w, npin = xd.n * hw;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
         acc += __ldg(dc + (int64_t)(ky * kw + kx) * col_sk + oy * ow + ox);
       }
     }
-    const int64_t o = z * x_sb + img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
-    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-    dx[o] = acc;
+    const int64_t o = img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    dx[z * x_sb + o] = acc;
   }
 }
 
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, es
 __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                        const int32_t* __restrict__ amax,
-                                                       const float* __restrict__ mask, int k, int stride, int pad) {
+                                                       const float* __restrict__ mask, int64_t mask_sb, int k,
+                                                       int stride, int pad) {
   const int z = blockIdx.z;
   const int hw = xd.h * xd.w, npin = xd.n * hw, ohw = yd.h * yd.w;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -208,9 +209,9 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
     for (int oy = oy_lo; oy <= oy_hi; ++oy)
       for (int ox = ox_lo; ox <= ox_hi; ++ox)
         if (ap[oy * yd.w + ox] == p) acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
-    const int64_t o = z * x_sb + img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
-    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-    dx[o] = acc;
+    const int64_t o = img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    dx[z * x_sb + o] = acc;
   }
 }
 
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(float* __restrict__ dx, esg
                                                      int64_t x_sb, const float* __restrict__ dy,
                                                      esgd_tensor4 yd, int64_t y_sb,
                                                      const int32_t* __restrict__ amax,
-                                                     const float* __restrict__ mask, int k,
+                                                     const float* __restrict__ mask, int64_t mask_sb, int k,
                                                      int stride, int pad) {
   const int z = blockIdx.y;
   const unsigned total = (unsigned)xd.n * xd.c * xd.h * xd.w;
@@ -274,9 +275,9 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(float* __restrict__ dx, esg
         const unsigned ye = (((unsigned)img * yd.c + c) * yd.h + oy) * yd.w + ox;
         if (amax[z * ytotal + ye] == me) acc += __ldg(dy + z * y_sb + off4(yd, img, c, oy, ox));
       }
-    const int64_t o = z * x_sb + off4(xd, img, c, iy, ix);
-    if (mask) acc = __fmul_rn(acc, mask[o] > 0.f ? 1.f : 0.f);
-    dx[o] = acc;
+    const int64_t o = off4(xd, img, c, iy, ix);
+    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    dx[z * x_sb + o] = acc;
   }
 }
 
@@ -372,7 +373,7 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
 extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dcol,
                                int64_t col_sp, int64_t col_sk, int64_t col_sb, int32_t kh, int32_t kw,
                                int32_t stride, int32_t pad, int32_t oh, int32_t ow, const float* mask,
-                               int32_t batch, esgd_stream_t stream) {
+                               int64_t mask_sb, int32_t batch, esgd_stream_t stream) {
   ESGD_REQUIRE(valid4(xd) && kh >= 1 && kw >= 1 && stride >= 1 && pad >= 0 && oh >= 1 &&
                    ow >= 1 && batch >= 1,
                ESGD_ERR_SHAPE, "col2im: bad geometry");
@@ -386,14 +387,14 @@ extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const f
     dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
     dim3 b2(256);
     if (stride == 1)
-      k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
+      k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb);
     else
-      k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
+      k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb);
     return check_launch("esgd_col2im_f32");
   }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
-  k_col2im<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sp, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask);
+  k_col2im<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sp, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb);
   return check_launch("esgd_col2im_f32");
 }
 
@@ -446,8 +447,8 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
 
 extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
                                     esgd_tensor4 yd, int64_t y_sb, const int32_t* argmax,
-                                    const float* mask, int32_t k, int32_t stride, int32_t pad,
-                                    int32_t batch, esgd_stream_t stream) {
+                                    const float* mask, int64_t mask_sb, int32_t k, int32_t stride,
+                                    int32_t pad, int32_t batch, esgd_stream_t stream) {
   ESGD_REQUIRE(valid4(xd) && valid4(yd) && k >= 1 && stride >= 1 && pad >= 0 && batch >= 1 &&
                    yd.n == xd.n && yd.c == xd.c,
                ESGD_ERR_SHAPE, "maxpool_bwd: bad geometry");
@@ -456,12 +457,12 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
   {
     dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
     dim3 b2(256);
-    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, k, stride, pad);
+    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad);
     return check_launch("esgd_maxpool_bwd_f32");
   }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
   dim3 grid(stride_grid(total, 256, 16), batch);
-  k_maxpool_bwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, k, stride, pad);
+  k_maxpool_bwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad);
   return check_launch("esgd_maxpool_bwd_f32");
 }
 

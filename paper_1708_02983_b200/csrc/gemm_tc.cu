@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <stdlib.h>
 #include <string.h>
 
 namespace esgd {
@@ -37,19 +38,22 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 32;                  // 32 fp32 = 128 B = one swizzle atom row
 constexpr int kThreads = 320;           // 10 warps: TMA, MMA, 4 split, 4 drain/epilogue
-constexpr int kChunkKB = 4;             // K-blocks (x32) per TMEM accumulation before promotion
+constexpr int kChunkKB = 2;             // K-blocks (x32) per TMEM accumulation before promotion
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
 template <int BN, bool SPLIT>
 struct Cfg {
   static constexpr int kTileBytesB = BN * BK * 4;
-  static constexpr int kStageBytes = (kTileBytesA + kTileBytesB) * (SPLIT ? 2 : 1);
-  static constexpr int kStages = SPLIT ? (BN >= 128 ? 3 : 4) : (BN >= 128 ? 6 : 8);
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
-  // stage layout: [A raw | A lo | B raw | B lo], every tile 1024-B aligned
-  static constexpr int kOffALo = kTileBytesA;
-  static constexpr int kOffB = SPLIT ? 2 * kTileBytesA : kTileBytesA;
+  // stage layout: [A raw | B raw | B lo (3xTF32)], every tile 1024-B aligned.
+  // In 3xTF32 mode A never gets a lo twin in smem: the split warps write the
+  // tf32 hi/lo rows of A straight into TMEM and the MMAs read A from there.
+  static constexpr int kOffB = kTileBytesA;
   static constexpr int kOffBLo = kOffB + kTileBytesB;
+  static constexpr int kStageBytes = kTileBytesA + kTileBytesB * (SPLIT ? 2 : 1);
+  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
+  static constexpr int kACol0 = 2 * BN;  // TMEM columns of the A regions (64 per stage: hi 32 | lo 32)
+  static constexpr int kTmemCols = SPLIT ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
+  static_assert(!SPLIT || kACol0 + 64 * kStages <= 512, "TMEM budget");
   static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
   static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -137,6 +141,26 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_c, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// A operand from TMEM ("TS"): K-major rows = TMEM lanes, 8 tf32 columns per MMA
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_c, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_c),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum), "r"(0u));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -174,6 +198,8 @@ struct Epi {
   float* ws;        // split-K partials [batch][splits][m][n]
   int splits, kb_per_split, batch;
   int out_mode;     // 0 direct stores, 1 TMA store M-contiguous C, 2 TMA store N-contiguous C
+  int m_fast;       // rasterise units m-fastest (M-contiguous output) else n-fastest
+  int dbg;          // diagnostics: 1 = stage but skip the bulk store, 2 = no read-wait
 };
 
 // epilogue value without the read-modify-write of accumulate (TMA-store path)
@@ -266,9 +292,17 @@ __device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, 
   int r = u - w.z * per_z;
   w.slice = r / (ntn * ntm);
   r -= w.slice * ntn * ntm;
-  // n fastest: consecutive CTAs share the A (M) tile in L2
-  w.m0 = (r / ntn) * BM;
-  w.n0 = (r % ntn) * BN_;
+  // Concurrent CTAs take neighbouring tiles along the output's contiguous
+  // dimension, so their stores (and the operand loads) stay within a few
+  // 2-MB pages: n-fastest ordering on an M-contiguous 600-MB output scattered
+  // 148 tiles over every page and throttled the stores to ~220 GB/s (TLB).
+  if (ep.m_fast) {
+    w.n0 = (r / ntm) * BN_;
+    w.m0 = (r % ntm) * BM;
+  } else {
+    w.m0 = (r / ntn) * BM;
+    w.n0 = (r % ntn) * BN_;
+  }
   w.kb0 = w.slice * ep.kb_per_split;
   w.nkb = max(0, min(nkb_all - w.kb0, ep.kb_per_split));
   return w;
@@ -336,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
       constexpr uint32_t idesc = idesc_tf32(BM, BN, AMN, BMN);
+      constexpr uint32_t idesc_ts = idesc_tf32(BM, BN, false, BMN);  // A from TMEM is K-major
       uint32_t g = 0, c = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
@@ -356,16 +391,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               // K-major: 8 tf32 = 32 B along K inside the swizzle atom;
               // MN-major: one 8-row K slab (1024 B) per instruction
-              const uint64_t ah = op_desc<AMN>(st, kk), bh = op_desc<BMN>(st + C::kOffB, kk);
+              const uint64_t bh = op_desc<BMN>(st + C::kOffB, kk);
               const uint32_t acc0 = (kb > kc || kk > 0) ? 1u : 0u;
               if (SPLIT) {
-                const uint64_t al = op_desc<AMN>(st + C::kOffALo, kk),
-                               bl = op_desc<BMN>(st + C::kOffBLo, kk);
-                mma_tf32(acc, al, bh, idesc, acc0);  // small terms first
-                mma_tf32(acc, ah, bl, idesc, 1u);
-                mma_tf32(acc, ah, bh, idesc, 1u);
+                const uint64_t bl = op_desc<BMN>(st + C::kOffBLo, kk);
+                const uint32_t ahi = tmem + C::kACol0 + s * 64 + kk * 8, alo = ahi + 32;
+                mma_tf32_ts(acc, alo, bh, idesc_ts, acc0);  // small terms first
+                mma_tf32_ts(acc, ahi, bl, idesc_ts, 1u);
+                mma_tf32_ts(acc, ahi, bh, idesc_ts, 1u);
               } else {
-                mma_tf32(acc, ah, bh, idesc, acc0);
+                mma_tf32(acc, op_desc<AMN>(st, kk), bh, idesc, acc0);
               }
             }
             mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
@@ -375,8 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp < 6) {
-    if (SPLIT) {  // ---- split warps: raw tile -> (hi in place, lo twin)
+    if (SPLIT) {
+      // ---- split warps: A row r (= TMEM lane) -> tf32 hi / lo in TMEM;
+      //      B tile -> hi in place + lo twin in smem
       const int et = threadIdx.x - 64;  // 0..127
+      const int q = warp & 3, r = q * 32 + lane;
       uint32_t g = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
@@ -384,9 +422,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % C::kStages;
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
-          split_tile<kTileBytesA>(st, st + C::kOffALo, et);
+          uint32_t hi[32], lo[32];
+          if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 x = lds4(st + r * 128 + ((c ^ (r & 7)) << 4));
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float h = tf32_hi(xs[e]);
+                hi[4 * c + e] = __float_as_uint(h);
+                lo[4 * c + e] = __float_as_uint(__fsub_rn(xs[e], h));
+              }
+            }
+          } else {  // MN-major SW128 boxes of 32(M) x 32(K): 4 KB per box, 16-B chunk (m%32)/4 ^ k%8
+            const uint32_t base = st + (r >> 5) * 4096 + ((r & 3) << 2);
+            const int c4 = (r & 31) >> 2;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              float x;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(base + k * 128 + ((c4 ^ (k & 7)) << 4)));
+              const float h = tf32_hi(x);
+              hi[k] = __float_as_uint(h);
+              lo[k] = __float_as_uint(__fsub_rn(x, h));
+            }
+          }
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + C::kACol0 + s * 64;
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
           split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(split0 + 8 * s);
         }
@@ -427,39 +494,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < BN; ++j)
             if (w.n0 + j < ep.n) P[w.n0 + j] = racc[j];
         }
+      } else if (ep.out_mode == 3) {
+        // diagnostic: compute but do not store (ESGD_DEBUG_NOSTORE=1)
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < BN; ++j) t += racc[j];
+        if (t == 12345.678f) ep.c[0] = t;
       } else if (ep.out_mode != 0) {
-        // smem-staged TMA store, 64 columns at a time
+        // smem-staged TMA store, 64 columns at a time. Branch-free fast path
+        // (no mask, identity/relu): one bias add, one max, one st.shared per
+        // element; the general epilogue (tanh/sigmoid/mask) only when needed.
         const uint32_t so = smem_u32(stage_out);
         float* cz = ep.c + w.z * ep.c_sb;
+        const bool fast = ep.mask == nullptr && (ep.act == ESGD_ACT_NONE || ep.act == ESGD_ACT_RELU);
+        const bool relu = ep.act == ESGD_ACT_RELU;
+        const float* bz = ep.bias ? ep.bias + w.z * ep.bias_sb : nullptr;
+        const int r = q * 32 + lane;
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h) {
           // staging buffer free? (previous bulk store has read it)
-          if (threadIdx.x == 192) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (threadIdx.x == 192 && ep.dbg != 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
           for (int jj = 0; jj < 64; jj += 4) {
-            float4 v;
             const int j = h * 64 + jj;
-            v.x = epi_value(ep, racc[j], w.z, row, w.n0 + j);
-            v.y = epi_value(ep, racc[j + 1], w.z, row, w.n0 + j + 1);
-            v.z = epi_value(ep, racc[j + 2], w.z, row, w.n0 + j + 2);
-            v.w = epi_value(ep, racc[j + 3], w.z, row, w.n0 + j + 3);
-            const int r = q * 32 + lane;
+            float v[4];
+            if (fast) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int col = w.n0 + j + e;
+                float x = racc[j + e];
+                if (bz) x = __fadd_rn(x, col < ep.n ? __ldg(bz + col) : 0.f);
+                v[e] = relu ? fmaxf(x, 0.f) : x;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) v[e] = epi_value(ep, racc[j + e], w.z, row, w.n0 + j + e);
+            }
             if (ep.out_mode == 1) {
               // M-contiguous output: staging [64 cols][128 rows], lanes walk rows
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 0) * 128 + r) * 4), "f"(v.x) : "memory");
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 1) * 128 + r) * 4), "f"(v.y) : "memory");
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 2) * 128 + r) * 4), "f"(v.z) : "memory");
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + 3) * 128 + r) * 4), "f"(v.w) : "memory");
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + e) * 128 + r) * 4), "f"(v[e]) : "memory");
             } else {
               // N-contiguous output: two 32-col boxes, 128-B rows, 128B swizzle
               const int box = jj >> 5, chunk = (jj & 31) >> 2;
-              sts4(so + box * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4), v);
+              sts4(so + box * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4), make_float4(v[0], v[1], v[2], v[3]));
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (threadIdx.x == 192) {
+          if (threadIdx.x == 192 && ep.dbg != 1) {
             const int ncol = w.n0 + h * 64;
             if (ep.out_mode == 1) {
               asm volatile(
@@ -481,8 +566,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          (void)cz;
         }
+        (void)cz;
       } else if (row < ep.m) {
         float* cz = ep.c + w.z * ep.c_sb;
 #pragma unroll
@@ -495,7 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (ep.out_mode != 0 && threadIdx.x == 192) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if ((ep.out_mode == 1 || ep.out_mode == 2) && threadIdx.x == 192)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -540,7 +626,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // 3-D map over an operand. K-major: dims (k, rows, batch), box (32, box_rows, 1).
 // MN-major: dims (rows, k, batch) with rows contiguous, box (32, 32, 1).
 int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64_t ld,
-             int64_t batch, int64_t sb, int box_rows, bool mn_major) {
+             int64_t batch, int64_t sb, int box_rows, bool mn_major, bool atom32 = true) {
   auto enc = get_encode();
   ESGD_REQUIRE(enc, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled unavailable");
   const int64_t inner = mn_major ? rows : k, outer = mn_major ? k : rows;
@@ -552,7 +638,7 @@ int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (mn_major && atom32) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   ESGD_REQUIRE(r == CUDA_SUCCESS, ESGD_ERR_CUDA, "tc_gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ESGD_OK;
@@ -566,7 +652,8 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: smem attribute: %s", cudaGetErrorString(e));
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN);
+  // 3xTF32: A is read by the split warps (not by UMMA), plain 128B swizzle
+  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN, /*atom32=*/!SPLIT);
   if (rc) return rc;
   rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN, BMN);
   if (rc) return rc;
@@ -610,8 +697,13 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) out_mode = 0;
   }
+  if (splits == 1 && getenv("ESGD_DEBUG_NOSTORE")) out_mode = 3;
+  const int m_fast = 0;  // (measured: m-fastest rasterisation was slower on every shape)
+  const char* dbg = getenv("ESGD_DEBUG_EPI");
+  const int dbg_mode = dbg ? atoi(dbg) : 0;
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
-         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch, out_mode};
+         d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch, out_mode,
+         m_fast, dbg_mode};
   // persistent: one CTA per SM (smem-limited), units dealt round-robin
   const int64_t units = (int64_t)tiles * splits;
   const int grid = (int)std::min<int64_t>(units, kNumSMs);

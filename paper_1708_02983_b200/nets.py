@@ -39,8 +39,11 @@ from .device import round_up
 from .errors import InputError, ShapeError
 from .network import Conv, ConvNetSpec, Dense, ModelSpec, Pool, view_table
 
-# a contraction goes to the tensor cores when M*N*K reaches this
-TC_MIN_FLOPS = 1 << 22
+import os
+
+# a contraction goes to the tensor cores when M*N*K reaches this (below it
+# the fixed cost of a persistent tcgen05 launch exceeds the FFMA kernel's)
+TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 22)))
 
 
 @dataclass
@@ -162,6 +165,7 @@ class DeviceNet:
             big = self.use_tc and L.kind == "dense" and b * fan_in * L.cout >= TC_MIN_FLOPS and fan_in >= 128
             self.dT.append(self._t(L.cout * round_up(b, 4)) if big else None)
         self.tc_calls = self.ffma_calls = 0
+        self.record = None  # list to capture (kind, descriptor, flops) of each GEMM launch
 
     def _out_desc(self, i: int) -> Tensor4:
         L = self.layers[i]
@@ -192,12 +196,16 @@ class DeviceNet:
                            a_major, b_major, self.tc_ws.data_ptr(), self.tc_ws.numel())
             _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream), "tc_gemm")
             self.tc_calls += 1
+            if self.record is not None:
+                self.record.append(("tc", d, 2.0 * m * n * k * nb))
         else:
             d = GemmDesc(m, n, k, nb, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
                          bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0,
                          self.gemm_ws.data_ptr(), self.gemm_ws.numel())
             _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream), "gemm")
             self.ffma_calls += 1
+            if self.record is not None:
+                self.record.append(("ffma", d, 2.0 * m * n * k * nb))
 
     # ---- passes ----------------------------------------------------------------
     def forward(self, W: torch.Tensor, stream: int, x: torch.Tensor | None = None) -> torch.Tensor:
@@ -337,8 +345,8 @@ class DeviceNet:
                 dnext = self._other(dcur)
                 mask = xin if pact == 1 else None
                 _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd, d_sb,
-                                                    self.amax[i].data_ptr(), mask, lay.k, lay.stride, lay.pad,
-                                                    nb, stream), "maxpool_bwd")
+                                                    self.amax[i].data_ptr(), mask, x_sb, lay.k, lay.stride,
+                                                    lay.pad, nb, stream), "maxpool_bwd")
                 dcur = dnext
             else:  # conv: delta is CNHW [Cout][np4]
                 lay = L.lay
@@ -367,5 +375,5 @@ class DeviceNet:
                 mask = xin if pact == 1 else None
                 _lib.check(lib.esgd_col2im_f32(dnext.data_ptr(), xd, dnext.stride(0), self.dcol.data_ptr(), 1,
                                                L.np4, self.dcol.stride(0), lay.k, lay.k, lay.stride, lay.pad,
-                                               L.hout, L.wout, mask, nb, stream), "col2im")
+                                               L.hout, L.wout, mask, x_sb, nb, stream), "col2im")
                 dcur = dnext

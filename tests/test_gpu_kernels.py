@@ -210,7 +210,7 @@ def test_im2col_col2im_adjoint_and_oracle():
     dx = torch.zeros((n, c, h, w), device="cuda")
     dcd = dev(dcol)
     _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dcd.data_ptr(), kp, 1, 0,
-              k, k, s, p, oh, ow, None, 1, stream_ptr())
+              k, k, s, p, oh, ow, None, 0, 1, stream_ptr())
     exp = O._col2im(dcol[:, :K].copy(), (n, c, h, w), k, s, p, oh, ow)
     assert np.array_equal(host(dx), exp)
 
@@ -232,7 +232,7 @@ def test_maxpool_fwd_bwd_vs_oracle():
     dx = torch.zeros((n, c, h, w), device="cuda")
     dyd = dev(dy)
     _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.nchw(n, c, h, w), 0, dyd.data_ptr(),
-              _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), None, k, s, p, 1, stream_ptr())
+              _lib.nchw(n, c, oh, ow), 0, am.data_ptr(), None, 0, k, s, p, 1, stream_ptr())
     assert np.array_equal(host(dx), O._maxpool_bwd(dy, ea, (n, c, h, w)))
 
 
@@ -291,7 +291,7 @@ def test_transposed_im2col_cnhw_and_rowsum():
     dd = dev(dcolT)
     dx = torch.zeros((c, plane), device="cuda")
     _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.cnhw(n, c, h, w, plane), 0, dd.data_ptr(), 1, np4, 0,
-              k, k, s, p, oh, ow, None, 1, stream_ptr())
+              k, k, s, p, oh, ow, None, 0, 1, stream_ptr())
     exp = O._col2im(dcolT[:, :npix].T.copy(), (n, c, h, w), k, s, p, oh, ow)
     assert np.array_equal(host(dx)[:, :n * h * w].reshape(c, n, h, w).transpose(1, 0, 2, 3), exp)
     rows = rng.standard_normal((7, 50000)).astype(np.float32)
