@@ -93,10 +93,20 @@ __global__ void __launch_bounds__(256) k_col2im(float* __restrict__ dx, esgd_ten
 // coalesced load and store (no per-element divisions) -------------------------
 constexpr int kGroup = 16;
 
+// channels / k values per thread: amortise the pixel decomposition over up to
+// kGroup of them, but keep >= ~2 waves of threads (small LeNet layers)
+inline int pick_group(int64_t pixels, int64_t count) {
+  const int64_t want_threads = (int64_t)kNumSMs * 2048;
+  int64_t g = (pixels * count) / want_threads;
+  if (g < 1) g = 1;
+  if (g > kGroup) g = kGroup;
+  return (int)g;
+}
+
 // transposed im2col colT[k][pix]
 __global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
                                                   const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
-                                                  int kh, int kw, int stride, int pad, int oh, int ow) {
+                                                  int kh, int kw, int stride, int pad, int oh, int ow, int grp) {
   const int z = blockIdx.z;
   const int np = xd.n * oh * ow, kdim = xd.c * kh * kw, khw = kh * kw;
   const int pix = blockIdx.x * blockDim.x + threadIdx.x;
@@ -105,7 +115,7 @@ __global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64
   const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
   const float* xz = x + z * x_sb + img * xd.sn;
   float* cz = col + z * col_sb + pix;
-  const int k0 = blockIdx.y * kGroup, k1 = min(kdim, k0 + kGroup);
+  const int k0 = blockIdx.y * grp, k1 = min(kdim, k0 + grp);
   int ci = k0 / khw, r = k0 - ci * khw, ky = r / kw, kx = r - ky * kw;
   for (int k = k0; k < k1; ++k) {
     const int iy = iy0 + ky, ix = ix0 + kx;
@@ -122,14 +132,14 @@ template <bool STRIDE1>
 __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                   const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                   int kh, int kw, int stride, int pad, int oh, int ow,
-                                                  const float* __restrict__ mask, int64_t mask_sb) {
+                                                  const float* __restrict__ mask, int64_t mask_sb, int grp) {
   const int z = blockIdx.z;
   const int hw = xd.h * xd.w, npin = xd.n * hw;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= npin) return;
   const int img = q / hw, p = q - img * hw, yh = p / xd.w, xw = p - yh * xd.w;
   const float* dz = dcol + z * col_sb + (int64_t)img * oh * ow;
-  const int c0 = blockIdx.y * kGroup, c1 = min(xd.c, c0 + kGroup);
+  const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
   for (int ci = c0; ci < c1; ++ci) {
     const float* dc = dz + (int64_t)(ci * kh * kw) * col_sk;
     float acc = 0.f;
@@ -155,14 +165,15 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
 // max pooling, thread <-> output pixel of the batch, channels of a group
 __global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
                                                        int32_t* __restrict__ amax, const float* __restrict__ x,
-                                                       esgd_tensor4 xd, int64_t x_sb, int k, int stride, int pad) {
+                                                       esgd_tensor4 xd, int64_t x_sb, int k, int stride, int pad,
+                                                       int grp) {
   const int z = blockIdx.z;
   const int ohw = yd.h * yd.w, np = yd.n * ohw;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= np) return;
   const int img = q / ohw, p = q - img * ohw, oy = p / yd.w, ox = p - oy * yd.w;
   const int64_t ytotal = (int64_t)yd.n * yd.c * ohw;
-  const int c0 = blockIdx.y * kGroup, c1 = min(yd.c, c0 + kGroup);
+  const int c0 = blockIdx.y * grp, c1 = min(yd.c, c0 + grp);
   for (int c = c0; c < c1; ++c) {
     const float* xp = x + z * x_sb + img * xd.sn + c * xd.sc;
     float best = -INFINITY;
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                        const int32_t* __restrict__ amax,
                                                        const float* __restrict__ mask, int64_t mask_sb, int k,
-                                                       int stride, int pad) {
+                                                       int stride, int pad, int grp) {
   const int z = blockIdx.z;
   const int hw = xd.h * xd.w, npin = xd.n * hw, ohw = yd.h * yd.w;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
   ox_lo = ox_lo <= 0 ? 0 : (ox_lo + stride - 1) / stride;
   int ox_hi = (ix + pad) / stride;
   if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
-  const int c0 = blockIdx.y * kGroup, c1 = min(xd.c, c0 + kGroup);
+  const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
   for (int c = c0; c < c1; ++c) {
     const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
     const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
@@ -357,9 +368,10 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
                "im2col: col strides must be (>=K, 1) or (1, >=pixels)");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "im2col: batch > 65535");
   ESGD_REQUIRE(col && x, ESGD_ERR_INPUT, "im2col: null buffer");
-  if (col_sp == 1 && (kdim + kGroup - 1) / kGroup <= 65535) {
-    dim3 g2((unsigned)((np + 255) / 256), (unsigned)((kdim + kGroup - 1) / kGroup), batch);
-    k_im2col_t<<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow);
+  const int gi = pick_group(np * batch, kdim);
+  if (col_sp == 1 && (kdim + gi - 1) / gi <= 65535) {
+    dim3 g2((unsigned)((np + 255) / 256), (unsigned)((kdim + gi - 1) / gi), batch);
+    k_im2col_t<<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, kh, kw, stride, pad, oh, ow, gi);
     return check_launch("esgd_im2col_f32");
   }
   dim3 grid(stride_grid(np * kdim, 256, 16), batch);
@@ -383,13 +395,14 @@ extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const f
   ESGD_REQUIRE(np * kdim < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED, "col2im: more than 2^31 elements");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "col2im: batch > 65535");
   ESGD_REQUIRE(dx && dcol, ESGD_ERR_INPUT, "col2im: null buffer");
-  if (col_sp == 1) {
-    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
+  const int gc = pick_group((int64_t)xd.n * xd.h * xd.w * batch, xd.c);
+  if (col_sp == 1 && (xd.c + gc - 1) / gc <= 65535) {
+    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gc - 1) / gc), batch);
     dim3 b2(256);
     if (stride == 1)
-      k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb);
+      k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb, gc);
     else
-      k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb);
+      k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb, gc);
     return check_launch("esgd_col2im_f32");
   }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
@@ -406,7 +419,7 @@ extern "C" int esgd_rowsum_f32(float* out, int64_t out_sb, const float* x, int64
   ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "rowsum: null buffer");
   ESGD_REQUIRE(rows <= 65535 && batch <= 65535, ESGD_ERR_UNSUPPORTED, "rowsum: grid too large");
   // ~2 CTAs per SM overall, chunks of >= 4096 elements
-  int64_t nchunk = (2 * kNumSMs + (int64_t)rows * batch - 1) / ((int64_t)rows * batch);
+  int64_t nchunk = (2 * kNumSMs + (int64_t)rows - 1) / (int64_t)rows;  // batch-independent order
   int64_t maxc = (cols + 4095) / 4096;
   if (nchunk > maxc) nchunk = maxc;
   if (nchunk > 64) nchunk = 64;
@@ -434,9 +447,10 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(y && argmax && x, ESGD_ERR_INPUT, "maxpool_fwd: null buffer");
   {
-    dim3 g2((unsigned)(((int64_t)yd.n * yd.h * yd.w + 255) / 256), (unsigned)((yd.c + kGroup - 1) / kGroup), batch);
+    const int gp = pick_group((int64_t)yd.n * yd.h * yd.w * batch, yd.c);
+    dim3 g2((unsigned)(((int64_t)yd.n * yd.h * yd.w + 255) / 256), (unsigned)((yd.c + gp - 1) / gp), batch);
     dim3 b2(256);
-    k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad);
+    k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad, gp);
     return check_launch("esgd_maxpool_fwd_f32");
   }
   int64_t total = (int64_t)yd.n * yd.c * yd.h * yd.w;
@@ -455,9 +469,10 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(dx && dy && argmax, ESGD_ERR_INPUT, "maxpool_bwd: null buffer");
   {
-    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + kGroup - 1) / kGroup), batch);
+    const int gp = pick_group((int64_t)xd.n * xd.h * xd.w * batch, xd.c);
+    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);
     dim3 b2(256);
-    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad);
+    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad, gp);
     return check_launch("esgd_maxpool_bwd_f32");
   }
   int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;

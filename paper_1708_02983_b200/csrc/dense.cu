@@ -329,7 +329,9 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
   if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
   ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
   ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
-  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
+  // the K split depends on the per-entry problem only (never on `batch`):
+  // replicas compute bit-identical results whatever the launch groups them with
+  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM);
   int splits = 1;
   if (d->ws && tiles < 2 * kNumSMs && d->k >= 4 * BK * 4) {
     // enough slices to give ~2 CTAs per SM, each slice at least 4 slabs deep
@@ -337,8 +339,8 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
     int maxs = d->k / (4 * BK);
     splits = want < maxs ? want : maxs;
     if (splits > 64) splits = 64;
-    while (splits > 1 && (int64_t)splits * d->m * d->n * d->batch > d->ws_floats) --splits;
-    if ((int64_t)d->batch * splits > 65535) splits = 1;
+    if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats || (int64_t)d->batch * splits > 65535)
+      splits = 1;
   }
   const int kchunk = ((d->k + splits - 1) / splits + BK - 1) / BK * BK;
   if (splits > 1) splits = (d->k + kchunk - 1) / kchunk;
@@ -395,10 +397,11 @@ extern "C" int esgd_colsum_f32(float* out, int64_t out_sb, const float* x, int64
   ESGD_REQUIRE(rows >= 1 && cols >= 1 && batch >= 1 && ld >= cols, ESGD_ERR_SHAPE,
                "colsum: bad shape");
   ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "colsum: null buffer");
-  // ~2 CTAs per SM over the whole reduction, chunks of >= 128 rows
+  // ~2 CTAs per SM per batch entry, chunks of >= 128 rows (batch-independent
+  // chunking keeps each entry's sum order fixed)
   int64_t col_groups = (cols + 31) / 32;
   int64_t nchunk = (rows + 127) / 128;
-  int64_t cap = (2 * kNumSMs + col_groups * batch - 1) / (col_groups * batch);
+  int64_t cap = (2 * kNumSMs + col_groups - 1) / col_groups;
   if (nchunk > cap) nchunk = cap;
   if (nchunk > 256) nchunk = 256;
   if (nchunk < 1) nchunk = 1;

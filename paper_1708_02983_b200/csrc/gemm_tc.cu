@@ -658,16 +658,19 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN, BMN);
   if (rc) return rc;
   const int nkb = (d->k + BK - 1) / BK;
-  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
+  // the K split depends on the per-entry problem only (not on `batch`), so a
+  // replica computes bit-identical results however many replicas share the
+  // launch — runs are reproducible across GPU counts
+  const int tiles_z = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM);
+  const int tiles = tiles_z * d->batch;
   // split K when the output tiles cannot fill the 148 SMs (weight gradients
-  // reduce over every pixel of the batch): ~2 waves, >= 4 chunks per slice
+  // reduce over every pixel of the batch): ~2 waves, >= 2 chunks per slice
   int splits = 1;
-  if (d->ws && tiles < kNumSMs && nkb >= 2 * kChunkKB) {
-    splits = (2 * kNumSMs) / tiles;
+  if (d->ws && tiles_z < kNumSMs && nkb >= 2 * kChunkKB) {
+    splits = (2 * kNumSMs) / tiles_z;
     splits = std::min(splits, nkb / (2 * kChunkKB));
     splits = std::min(splits, 128);
-    while (splits > 1 && (int64_t)splits * d->m * d->n * d->batch > d->ws_floats) --splits;
-    if ((int64_t)d->batch * splits > 65535) splits = 1;
+    if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats) splits = 1;  // never batch-dependent
     if (splits < 1) splits = 1;
   }
   int kbps = (nkb + splits - 1) / splits;

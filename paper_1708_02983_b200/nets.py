@@ -43,7 +43,9 @@ import os
 
 # a contraction goes to the tensor cores when M*N*K reaches this (below it
 # the fixed cost of a persistent tcgen05 launch exceeds the FFMA kernel's)
-TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 22)))
+# (measured on B200: LeNet's <=1e8-MAC GEMMs are faster on the split-K FFMA
+# kernel, every AlexNet contraction (>=5e8 MACs) on tcgen05)
+TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 28)))
 
 
 @dataclass

@@ -1,0 +1,21 @@
+"""Multi-GPU Sync EASGD (one process per GPU, NCCL allreduce captured in the
+round's CUDA graph) — runs only where >= 2 GPUs are visible; equality with
+the single-process run is bitwise at N = 2 (tools/dist_check.py)."""
+
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_two_rank_sync_easgd_equals_single_process():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "tools" / "dist_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert "DIST_CHECK PASS" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -51,19 +51,30 @@ def _cnn_case(spec, layers, n, b, seed=0):
     return g_dev, g_ref
 
 
-def test_lenet_gradient_vs_oracle():
+@pytest.fixture(params=["tcgen05", "default"])
+def gemm_routing(request, monkeypatch):
+    """'tcgen05' sends every contraction above 4M MACs to the tensor-core
+    kernel (so small test batches exercise it); 'default' is the engine's
+    production routing."""
+    from paper_1708_02983_b200 import nets
+    if request.param == "tcgen05":
+        monkeypatch.setattr(nets, "TC_MIN_FLOPS", 1 << 22)
+    return request.param
+
+
+def test_lenet_gradient_vs_oracle(gemm_routing):
     g_dev, g_ref = _cnn_case(network.lenet(), O.LENET, 300, 16)
     assert rel_err(g_dev, g_ref) < TOL
 
 
-def test_cifar_quick_gradient_vs_oracle():
+def test_cifar_quick_gradient_vs_oracle(gemm_routing):
     g_dev, g_ref = _cnn_case(network.cifar_quick(), O.CIFAR_QUICK, 200, 8)
     assert rel_err(g_dev, g_ref) < TOL
 
 
-def test_alexnet_gradient_vs_oracle():
-    """full AlexNet geometry (61.1M params) at a small batch: exercises the
-    tcgen05 3xTF32 GEMMs on every conv / fc contraction that qualifies."""
+def test_alexnet_gradient_vs_oracle(gemm_routing):
+    """full AlexNet geometry (61.1M params) at a small batch: with the
+    tcgen05 routing every conv / fc contraction runs on the 3xTF32 kernel."""
     spec = network.alexnet(num_classes=1000)
     g_dev, g_ref = _cnn_case(spec, O.alexnet_layers(1000), 6, 2)
     assert rel_err(g_dev, g_ref) < TOL

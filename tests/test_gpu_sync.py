@@ -89,14 +89,17 @@ def test_quadratic_converges():
 
 
 @pytest.mark.parametrize("model", ["lenet", "cifar-quick"])
-def test_sync_cnn_multi_replica_vs_oracle(model):
+@pytest.mark.parametrize("tc", [True, False])
+def test_sync_cnn_multi_replica_vs_oracle(model, tc, monkeypatch):
     """P workers as batched replicas of one DeviceNet (every CNN kernel runs
     with batch = P) against the oracle's sequential workers. Three rounds of a
     randomly-initialised CNN on random data amplify the ~3e-6 per-gradient
     difference of the tensor-core path, hence 1e-4 here (one-gradient parity
     is held to 1e-5 in test_gpu_network.py)."""
-    from paper_1708_02983_b200 import network
+    from paper_1708_02983_b200 import network, nets
 
+    if tc:
+        monkeypatch.setattr(nets, "TC_MIN_FLOPS", 1 << 22)
     spec = network.MODELS[model](seed=1)
     layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK}[model]
     rng = np.random.default_rng(7)

@@ -30,8 +30,9 @@ def main():
     cfg = make_config("sync-easgd3", workers=P, iterations=12, batch_size=32,
                       hyper=HyperParams(eta=0.05, rho=0.25), eval_every=6, seed=3)
     rec = run_trainer(cfg, prob)
+    torch.cuda.synchronize()
+    dist.barrier()
     if rank == 0:
-        dist.destroy_process_group()
         # the same run in one process (all P workers on this GPU)
         ref = run_trainer(cfg, prob)
         err = float(np.linalg.norm(rec.final_weights - ref.final_weights) / np.linalg.norm(ref.final_weights))
@@ -39,10 +40,14 @@ def main():
                    for a, b in zip(rec.final_worker_weights, ref.final_worker_weights))
         print(f"world={world} P={P} center rel err {err:.3e} worker max rel err {werr:.3e} "
               f"bitwise={rec.weights_digest == ref.weights_digest} graph={rec.engine_info.get('graph')}")
-        ok = err < 1e-6 and werr < 1e-6
+        # every kernel's decomposition is independent of how many replicas a
+        # launch carries, and a two-rank NCCL sum is order-free: bitwise at N=2
+        ok = (rec.weights_digest == ref.weights_digest) if world == 2 else (err < 1e-6 and werr < 1e-6)
         print("DIST_CHECK", "PASS" if ok else "FAIL")
-        sys.exit(0 if ok else 1)
-    dist.destroy_process_group()
+        sys.stdout.flush()
+        os._exit(0 if ok else 1)
+    sys.stdout.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":
