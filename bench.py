@@ -284,21 +284,26 @@ def run_device(args):
 
 
 def launches_per_step(eng) -> int:
-    """Kernels of libesgd per round (counted from the layer plan)."""
-    net = getattr(eng.plan, "net", None)
-    if net is None:
-        return 3
-    k = 1  # sample
-    for L in net.layers:
-        if L.kind == "conv":
-            k += 2 + 2 + (2 if L is not net.layers[0] else 0)  # im2col+gemm ; wgrad+colsum ; dgrad+col2im
-        elif L.kind == "pool":
-            k += 2
-        else:
-            k += 1 + (1 if L.flatten_in else 0) + 2 + 1
-    k += 1  # softmax
-    k += 2  # replica sum + update
-    return k
+    """libesgd kernels in one round, counted from a CUPTI trace of one eager
+    round (torch.profiler; outside the timed region)."""
+    import torch
+
+    from paper_1708_02983_b200.device import stream_ptr
+
+    W, G = eng.W.clone(), eng.G.clone()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        eng.plan.gradient(G, W, stream_ptr())
+        from paper_1708_02983_b200.fabric.collectives import replica_sum_
+        replica_sum_(eng.S.clone(), W, eng.n)
+        from paper_1708_02983_b200.updates import sync_update_
+        sync_update_(W, G, eng.C.clone(), eng.S.clone(), eng.n, eng.P, eng.cfg.hyper)
+        torch.cuda.synchronize()
+    n = 0
+    for e in prof.events():
+        if getattr(e, "device_type", None) is not None and "esgd" in e.name and "Memcpy" not in e.name:
+            if str(e.device_type).endswith("CUDA"):
+                n += 1
+    return n
 
 
 def run_e2e(args, spec, train, cfg, world):
@@ -327,7 +332,7 @@ def run_e2e(args, spec, train, cfg, world):
     b = cfg.batch_size
     return {"value": round(args.steps * cfg.cluster.workers * b / dt, 1), "unit": "samples/s",
             "h2d_bytes_per_step": stager.h2d_bytes, "d2h_bytes_per_step": stager.d2h_bytes,
-            "path": "host SplitMix64 sampling -> pinned batch -> H2D -> round -> loss D2H"}
+            "path": "host SplitMix64 sampling + gather -> pinned batch -> (graph: H2D, round, loss D2H) -> sync"}
 
 
 class HostStager:
@@ -352,18 +357,16 @@ class HostStager:
         self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
         self.h2d_bytes = self.hx.numel() * 4 + self.hy.numel() * 4
         self.d2h_bytes = nrep * 4
+        self.graph, self.use_graph = None, True
 
-    def step(self):
+    def _device_round(self):
+        """H2D of the staged batch, the round, D2H of the mean loss — all
+        stream-ordered so the whole thing can be captured in one graph."""
         import torch
 
         from paper_1708_02983_b200.device import stream_ptr
 
         eng, net = self.eng, self.net
-        hx, hy = self.hx.numpy(), self.hy.numpy()
-        for r, rng in enumerate(self.rngs):
-            idx = rng.randint_block(net.b, self.X.shape[0])
-            np.take(self.X, idx, axis=0, out=hx[r].reshape(net.b, net.d_in))
-            hy[r] = self.Y[idx]
         net.x.copy_(self.hx, non_blocking=True)
         net.y.copy_(self.hy, non_blocking=True)
         cs = torch.cuda.current_stream()
@@ -374,7 +377,36 @@ class HostStager:
         cs.wait_stream(eng.comm)
         eng._update(cs)
         self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
-        cs.synchronize()
+
+    def _stage_host(self):
+        hx, hy = self.hx.numpy(), self.hy.numpy()
+        net = self.net
+        for r, rng in enumerate(self.rngs):
+            idx = rng.randint_block(net.b, self.X.shape[0])
+            np.take(self.X, idx, axis=0, out=hx[r].reshape(net.b, net.d_in))
+            hy[r] = self.Y[idx]
+
+    def step(self):
+        import torch
+
+        self._stage_host()
+        if self.graph is None and self.use_graph:
+            try:
+                g = torch.cuda.CUDAGraph()
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+                    self._device_round()
+                torch.cuda.current_stream().wait_stream(s)
+                self.graph = g
+            except Exception:
+                self.use_graph = False
+                torch.cuda.synchronize()
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._device_round()
+        torch.cuda.current_stream().synchronize()
         return float(self.loss.numpy().mean())
 
 

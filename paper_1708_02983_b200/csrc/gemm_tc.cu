@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < BN; ++j) t += racc[j];
         if (t == 12345.678f) ep.c[0] = t;
       } else if (ep.out_mode != 0) {
-        // smem-staged TMA store, 64 columns at a time. Branch-free fast path
+        // smem-staged TMA store, 32 columns (16 KB) at a time through a
+        // two-slot ring, so staging quarter q+1 overlaps the bulk store of q. Branch-free fast path
         // (no mask, identity/relu): one bias add, one max, one st.shared per
         // element; the general epilogue (tanh/sigmoid/mask) only when needed.
         const uint32_t so = smem_u32(stage_out);
@@ -511,13 +512,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* bz = ep.bias ? ep.bias + w.z * ep.bias_sb : nullptr;
         const int r = q * 32 + lane;
 #pragma unroll
-        for (int h = 0; h < BN / 64; ++h) {
-          // staging buffer free? (previous bulk store has read it)
-          if (threadIdx.x == 192 && ep.dbg != 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        for (int qd = 0; qd < BN / 32; ++qd) {
+          const uint32_t sb = so + (qd & 1) * 16384;
+          // slot free? (the store issued two quarters ago has read it)
+          if (threadIdx.x == 192 && ep.dbg != 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
-          for (int jj = 0; jj < 64; jj += 4) {
-            const int j = h * 64 + jj;
+          for (int jj = 0; jj < 32; jj += 4) {
+            const int j = qd * 32 + jj;
             float v[4];
             if (fast) {
 #pragma unroll
@@ -532,38 +534,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < 4; ++e) v[e] = epi_value(ep, racc[j + e], w.z, row, w.n0 + j + e);
             }
             if (ep.out_mode == 1) {
-              // M-contiguous output: staging [64 cols][128 rows], lanes walk rows
+              // M-contiguous output: slot [32 cols][128 rows], lanes walk rows
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(so + ((jj + e) * 128 + r) * 4), "f"(v[e]) : "memory");
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((jj + e) * 128 + r) * 4), "f"(v[e]) : "memory");
             } else {
-              // N-contiguous output: two 32-col boxes, 128-B rows, 128B swizzle
-              const int box = jj >> 5, chunk = (jj & 31) >> 2;
-              sts4(so + box * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4), make_float4(v[0], v[1], v[2], v[3]));
+              // N-contiguous output: one 32-col box, 128-B rows, 128B swizzle
+              sts4(sb + r * 128 + (((jj >> 2) ^ (r & 7)) << 4), make_float4(v[0], v[1], v[2], v[3]));
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (threadIdx.x == 192 && ep.dbg != 1) {
-            const int ncol = w.n0 + h * 64;
-            if (ep.out_mode == 1) {
+            const int ncol = w.n0 + qd * 32;
+            if (ep.out_mode == 1)
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(w.m0), "r"(ncol), "r"(w.z), "r"(so)
+                  "r"(w.m0), "r"(ncol), "r"(w.z), "r"(sb)
                   : "memory");
-            } else {
+            else
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(ncol), "r"(w.m0), "r"(w.z), "r"(so)
+                  "r"(ncol), "r"(w.m0), "r"(w.z), "r"(sb)
                   : "memory");
-              asm volatile(
-                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                      reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(ncol + 32), "r"(w.m0), "r"(w.z), "r"(so + 16384)
-                  : "memory");
-            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
@@ -693,7 +688,7 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
     bstride = (bstride + 3) & ~int64_t(3);
     cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)d->batch};
     cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
-    cuuint32_t box[3] = {mcont ? 128u : 32u, mcont ? 64u : 128u, 1};
+    cuuint32_t box[3] = {mcont ? 128u : 32u, mcont ? 32u : 128u, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d->c, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, mcont ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,

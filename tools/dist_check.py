@@ -33,6 +33,9 @@ def main():
     torch.cuda.synchronize()
     dist.barrier()
     if rank == 0:
+        # the run's engine (and its captured NCCL graph) is gone; leave the
+        # group so the reference run below is a plain single-process run
+        dist.destroy_process_group()
         # the same run in one process (all P workers on this GPU)
         ref = run_trainer(cfg, prob)
         err = float(np.linalg.norm(rec.final_weights - ref.final_weights) / np.linalg.norm(ref.final_weights))
