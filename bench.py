@@ -336,11 +336,16 @@ def run_e2e(args, spec, train, cfg, world):
 
 
 class HostStager:
-    """Host data path: each round the local workers' batches are drawn with
-    the same SplitMix64 streams on the host, gathered into pinned memory,
-    copied to the device, and the round's mean loss is read back."""
+    """Host data path of the e2e measurement, pipelined like a data loader:
+    each round's batches are drawn on the host with the workers' SplitMix64
+    streams and gathered (thread pool) into one of two pinned buffers while
+    the device runs the previous round; one CUDA graph per buffer does the
+    H2D copy, the round and the D2H of the round's mean loss, which is read
+    back after every round."""
 
-    def __init__(self, prob, eng):
+    def __init__(self, prob, eng, threads: int = 8):
+        import concurrent.futures as cf
+
         import torch
 
         from paper_1708_02983_b200.rng import CounterRng, stream_seed
@@ -352,23 +357,45 @@ class HostStager:
         self.X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
         self.Y = prob.train.labels.astype(np.int32)
         self.rngs = [CounterRng(stream_seed(eng.cfg.seed, w)) for w in range(eng.first, eng.first + nrep)]
-        self.hx = torch.empty((nrep, b * d), dtype=torch.float32).pin_memory()
-        self.hy = torch.empty((nrep, b), dtype=torch.int32).pin_memory()
+        self.hx = [torch.empty((nrep, b * d), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.hy = [torch.empty((nrep, b), dtype=torch.int32).pin_memory() for _ in range(2)]
         self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
-        self.h2d_bytes = self.hx.numel() * 4 + self.hy.numel() * 4
+        self.h2d_bytes = self.hx[0].numel() * 4 + self.hy[0].numel() * 4
         self.d2h_bytes = nrep * 4
-        self.graph, self.use_graph = None, True
+        self.graphs = [None, None]
+        self.pool = cf.ThreadPoolExecutor(max_workers=threads)
+        self.cur = 0
+        self.pending = self.pool.submit(self._stage_host, 0)
+        self.inflight = False
 
-    def _device_round(self):
-        """H2D of the staged batch, the round, D2H of the mean loss — all
-        stream-ordered so the whole thing can be captured in one graph."""
+    def _gather(self, dst, idx):
+        np.take(self.X, idx, axis=0, out=dst)
+
+    def _stage_host(self, k):
+        hx, hy = self.hx[k].numpy(), self.hy[k].numpy()
+        net = self.net
+        jobs = []
+        for r, rng in enumerate(self.rngs):
+            idx = rng.randint_block(net.b, self.X.shape[0])
+            hy[r] = self.Y[idx]
+            rows = hx[r].reshape(net.b, net.d_in)
+            step = max(1, net.b // 8)
+            for lo in range(0, net.b, step):  # big rows: gather in parallel chunks
+                jobs.append((rows[lo:lo + step], idx[lo:lo + step]))
+        if len(jobs) > 1 and self.X.shape[1] >= 4096:
+            list(self.pool.map(lambda j: self._gather(*j), jobs))
+        else:
+            for dst, idx in jobs:
+                self._gather(dst, idx)
+
+    def _device_round(self, k):
         import torch
 
         from paper_1708_02983_b200.device import stream_ptr
 
         eng, net = self.eng, self.net
-        net.x.copy_(self.hx, non_blocking=True)
-        net.y.copy_(self.hy, non_blocking=True)
+        net.x.copy_(self.hx[k], non_blocking=True)
+        net.y.copy_(self.hy[k], non_blocking=True)
         cs = torch.cuda.current_stream()
         eng.comm.wait_stream(cs)
         with torch.cuda.stream(eng.comm):
@@ -378,35 +405,28 @@ class HostStager:
         eng._update(cs)
         self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
 
-    def _stage_host(self):
-        hx, hy = self.hx.numpy(), self.hy.numpy()
-        net = self.net
-        for r, rng in enumerate(self.rngs):
-            idx = rng.randint_block(net.b, self.X.shape[0])
-            np.take(self.X, idx, axis=0, out=hx[r].reshape(net.b, net.d_in))
-            hy[r] = self.Y[idx]
+    def _graph(self, k):
+        import torch
+
+        if self.graphs[k] is None:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+                self._device_round(k)
+            torch.cuda.current_stream().wait_stream(s)
+            self.graphs[k] = g
+        return self.graphs[k]
 
     def step(self):
         import torch
 
-        self._stage_host()
-        if self.graph is None and self.use_graph:
-            try:
-                g = torch.cuda.CUDAGraph()
-                s = torch.cuda.Stream()
-                s.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
-                    self._device_round()
-                torch.cuda.current_stream().wait_stream(s)
-                self.graph = g
-            except Exception:
-                self.use_graph = False
-                torch.cuda.synchronize()
-        if self.graph is not None:
-            self.graph.replay()
-        else:
-            self._device_round()
+        k = self.cur
+        self.pending.result()                                # batch k staged on the host
+        self._graph(k).replay()                              # H2D + round + loss D2H (async)
+        self.pending = self.pool.submit(self._stage_host, k ^ 1)  # stage the next batch meanwhile
         torch.cuda.current_stream().synchronize()
+        self.cur = k ^ 1
         return float(self.loss.numpy().mean())
 
 

@@ -139,10 +139,33 @@ def trainer_fixture():
     return d
 
 
+def async_fixture():
+    """Loss curves of the reference's async / Hogwild schedules on the MLP
+    problem (simulated engine, FCFS by virtual time) for statistical parity."""
+    d = {}
+    train = normalize(gen_synthetic(10, 32, 40, seed=5, separation=5.0))
+    test = normalize(gen_synthetic(10, 32, 10, seed=6, separation=5.0))
+    spec = ModelSpec((32, 24, 16, 10), activation="relu", seed=1, dtype=np.float32)
+    prob = NetworkProblem(spec, train, test)
+    cm = CostModel.preset("fdr")
+    for method, hy in (("async-measgd", HyperParams(eta=0.02, rho=0.25, mu=0.9)),
+                       ("async-easgd", HyperParams(eta=0.05, rho=0.25)),
+                       ("hogwild-easgd", HyperParams(eta=0.05, rho=0.25))):
+        rec = run_trainer(make_config(method, workers=4, iterations=800, batch_size=16, hyper=hy,
+                                      eval_every=200, seed=3), prob, cm)
+        d[f"{method}_loss"] = np.array(rec.train_loss)
+        d[f"{method}_acc"] = np.array(rec.test_accuracy)
+    d["init_loss"] = np.array([prob.train_loss(prob.init_weights())])
+    return d
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    only = sys.argv[1:]
     for name, fn in (("rng", rng_fixture), ("data", data_fixture), ("updates", update_fixture),
-                     ("net", net_fixture), ("trainers", trainer_fixture)):
+                     ("net", net_fixture), ("trainers", trainer_fixture), ("async", async_fixture)):
+        if only and name not in only:
+            continue
         path = OUT / f"{name}.npz"
         np.savez_compressed(path, **fn())
         print(path, path.stat().st_size)

@@ -34,9 +34,12 @@ __device__ __forceinline__ float act_grad_mul(float d, float z, int act) {
 }
 
 // ---- strided batched FFMA GEMM ---------------------------------------------
-// 64x64 output tile per 256-thread CTA, 4x4 per thread, BK=16 slabs staged
-// through shared memory (A transposed so the inner loop reads float4 rows).
-constexpr int BM = 64, BN = 64, BK = 16;
+// TBM x TBN output tile per 256-thread CTA (16x16 threads, (TBM/16)x(TBN/16)
+// per thread), BK=16 slabs staged through shared memory (A transposed so the
+// inner loop reads contiguous rows). 64x64 for large outputs, 32x32 when the
+// output is skinny (weight gradients of small layers) so more CTAs share the
+// split-K reduction.
+constexpr int BK = 16;
 
 __device__ __forceinline__ float epilogue(const esgd_gemm_desc& d, float acc, int z, int gm, int gn,
                                           float* C, float* Cp, int64_t off) {
@@ -54,48 +57,58 @@ __device__ __forceinline__ float epilogue(const esgd_gemm_desc& d, float acc, in
 // splits > 1: blockIdx.z = batch * splits + slice; each slice reduces its own
 // k range and writes raw partials to ws[z][slice][m][n]; k_gemm_reduce
 // combines slices in order and applies the epilogue.
+template <int TBM, int TBN>
 __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d, int splits, int kchunk) {
-  __shared__ __align__(16) float As[2][BK][BM + 4];
-  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  constexpr int MI = TBM / 16, NI = TBN / 16, LA = TBM * BK / 256, LB = TBN * BK / 256;
+  __shared__ __align__(16) float As[2][BK][TBM + 4];
+  __shared__ __align__(16) float Bs[2][BK][TBN + 4];
   const int z = blockIdx.z / splits, slice = blockIdx.z % splits;
   const int kbeg = slice * kchunk, kend = min(d.k, kbeg + kchunk);
   const float* A = d.a + z * d.a_sb;
   const float* B = d.b + z * d.b_sb;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * TBM, n0 = blockIdx.x * TBN;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const bool a_kfast = (d.a_sk == 1);
   const bool b_nfast = (d.b_sn == 1);
 
-  float acc[4][4];
+  float acc[MI][NI];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < NI; ++j) acc[i][j] = 0.f;
 
-  float ra[4], rb[4];
+  float ra[LA], rb[LB];
   auto load_regs = [&](int k0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < LA; ++j) {
       int e = tid + j * 256;
       int mm, kk;
-      if (a_kfast) { mm = e >> 4; kk = e & 15; } else { mm = e & 63; kk = e >> 6; }
+      if (a_kfast) { mm = e / BK; kk = e % BK; } else { mm = e % TBM; kk = e / TBM; }
       int gm = m0 + mm, gk = k0 + kk;
       ra[j] = (gm < d.m && gk < kend) ? __ldg(A + (int64_t)gm * d.a_sm + (int64_t)gk * d.a_sk) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < LB; ++j) {
+      int e = tid + j * 256;
       int nn, kb;
-      if (b_nfast) { nn = e & 63; kb = e >> 6; } else { nn = e >> 4; kb = e & 15; }
+      if (b_nfast) { nn = e % TBN; kb = e / TBN; } else { nn = e / BK; kb = e % BK; }
       int gn = n0 + nn, gkb = k0 + kb;
       rb[j] = (gn < d.n && gkb < kend) ? __ldg(B + (int64_t)gkb * d.b_sk + (int64_t)gn * d.b_sn) : 0.f;
     }
   };
   auto store_smem = [&](int buf) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < LA; ++j) {
       int e = tid + j * 256;
       int mm, kk;
-      if (a_kfast) { mm = e >> 4; kk = e & 15; } else { mm = e & 63; kk = e >> 6; }
+      if (a_kfast) { mm = e / BK; kk = e % BK; } else { mm = e % TBM; kk = e / TBM; }
       As[buf][kk][mm] = ra[j];
+    }
+#pragma unroll
+    for (int j = 0; j < LB; ++j) {
+      int e = tid + j * 256;
       int nn, kb;
-      if (b_nfast) { nn = e & 63; kb = e >> 6; } else { nn = e >> 4; kb = e & 15; }
+      if (b_nfast) { nn = e % TBN; kb = e / TBN; } else { nn = e / BK; kb = e % BK; }
       Bs[buf][kb][nn] = rb[j];
     }
   };
@@ -109,13 +122,15 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d, int splits, int 
     if (t + 1 < nk) load_regs(kbeg + (t + 1) * BK);  // prefetch next slab into registers
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float4 a4 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
-      float4 b4 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-      float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+      float av[MI], bv[NI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i) av[i] = As[buf][kk][ty * MI + i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      for (int j = 0; j < NI; ++j) bv[j] = Bs[buf][kk][tx * NI + j];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     if (t + 1 < nk) store_smem(buf ^ 1);
     __syncthreads();
@@ -124,12 +139,12 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d, int splits, int 
   if (splits > 1) {
     float* P = d.ws + ((int64_t)z * splits + slice) * d.m * d.n;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int gm = m0 + ty * 4 + i;
+    for (int i = 0; i < MI; ++i) {
+      int gm = m0 + ty * MI + i;
       if (gm >= d.m) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int gn = n0 + tx * 4 + j;
+      for (int j = 0; j < NI; ++j) {
+        int gn = n0 + tx * NI + j;
         if (gn < d.n) P[(int64_t)gm * d.n + gn] = acc[i][j];
       }
     }
@@ -138,12 +153,12 @@ __global__ void __launch_bounds__(256) k_gemm(esgd_gemm_desc d, int splits, int 
   float* C = d.c + z * d.c_sb;
   float* Cp = d.c_pre ? d.c_pre + z * d.c_sb : nullptr;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int gm = m0 + ty * 4 + i;
+  for (int i = 0; i < MI; ++i) {
+    int gm = m0 + ty * MI + i;
     if (gm >= d.m) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int gn = n0 + tx * 4 + j;
+    for (int j = 0; j < NI; ++j) {
+      int gn = n0 + tx * NI + j;
       if (gn >= d.n) continue;
       int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
       C[off] = epilogue(d, acc[i][j], z, gm, gn, C, Cp, off);
@@ -329,24 +344,29 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
   if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
   ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
   ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
+  // 32x32 tiles when 64x64 tiles cannot fill the machine (skinny outputs)
+  const int t64 = ((d->n + 63) / 64) * ((d->m + 63) / 64);
+  const bool small = t64 < kNumSMs;
+  const int TM = small ? 32 : 64, TN = TM;
   // the K split depends on the per-entry problem only (never on `batch`):
   // replicas compute bit-identical results whatever the launch groups them with
-  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM);
+  const int tiles = ((d->n + TN - 1) / TN) * ((d->m + TM - 1) / TM);
   int splits = 1;
   if (d->ws && tiles < 2 * kNumSMs && d->k >= 4 * BK * 4) {
     // enough slices to give ~2 CTAs per SM, each slice at least 4 slabs deep
     int want = (2 * kNumSMs + tiles - 1) / tiles;
     int maxs = d->k / (4 * BK);
     splits = want < maxs ? want : maxs;
-    if (splits > 64) splits = 64;
+    if (splits > 128) splits = 128;
     if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats || (int64_t)d->batch * splits > 65535)
       splits = 1;
   }
   const int kchunk = ((d->k + splits - 1) / splits + BK - 1) / BK * BK;
   if (splits > 1) splits = (d->k + kchunk - 1) / kchunk;
-  dim3 grid((d->n + BN - 1) / BN, (d->m + BM - 1) / BM, d->batch * splits);
+  dim3 grid((d->n + TN - 1) / TN, (d->m + TM - 1) / TM, d->batch * splits);
   ESGD_REQUIRE(grid.y <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: m too large for the FFMA path");
-  k_gemm<<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
+  if (small) k_gemm<32, 32><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
+  else k_gemm<64, 64><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
   if (splits > 1) {
     dim3 rgrid(stride_grid((int64_t)d->m * d->n, 256, 4), d->batch);
     k_gemm_reduce<<<rgrid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits);

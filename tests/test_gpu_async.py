@@ -72,3 +72,25 @@ def test_async_measgd_statistical_parity_with_reference(golden):
     ours = prob.distance_to_optimum(rec.final_weights)
     ref = float(g["quad_async-measgd_dist"][0])
     assert ours < max(10 * ref, 1e-2), (ours, ref)
+
+
+@pytest.mark.parametrize("method,eta,mu", [("async-measgd", 0.02, 0.9), ("async-easgd", 0.05, 0.9),
+                                           ("hogwild-easgd", 0.05, 0.9)])
+def test_async_loss_curve_parity_with_reference(golden, method, eta, mu):
+    """Statistical parity (the schedules race / are FCFS by real time): same
+    MLP problem, seeds and budget as the reference's run; the device run must
+    learn as well (final loss and accuracy within a band of the reference's)."""
+    from paper_1708_02983_b200 import ModelSpec
+    from paper_1708_02983_b200.datasets import Dataset
+    from paper_1708_02983_b200.trainers import NetworkProblem
+
+    g, net = golden("async"), golden("net")
+    spec = ModelSpec((32, 24, 16, 10), activation="relu", seed=1, dtype=np.float32)
+    prob = NetworkProblem(spec, Dataset(net["train_x"], net["train_y"], 10), Dataset(net["test_x"], net["test_y"], 10))
+    rec = run_trainer(make_config(method, workers=4, iterations=800, batch_size=16,
+                                  hyper=HyperParams(eta=eta, rho=0.25, mu=mu), eval_every=200, seed=3), prob)
+    ref_loss, ref_acc = g[f"{method}_loss"], g[f"{method}_acc"]
+    assert len(rec.train_loss) == len(ref_loss)
+    assert rec.train_loss[-1] <= max(1.5 * ref_loss[-1], ref_loss[-1] + 0.15), (rec.train_loss, ref_loss)
+    assert rec.test_accuracy[-1] >= ref_acc[-1] - 0.1, (rec.test_accuracy, ref_acc)
+    assert rec.train_loss[-1] < float(g["init_loss"][0])

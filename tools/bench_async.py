@@ -32,7 +32,9 @@ def main():
     spec = network.MODELS[args.model](seed=0)
     train, _ = bench.make_data(args.model, spec)
     prob = NetworkProblem(spec, train)
-    hy = HyperParams(eta=wl["eta"], rho=wl["rho"], mu=0.9)
+    # momentum methods: eta scaled by (1 - mu) so the effective step matches the sync runs
+    eta = wl["eta"] * (0.1 if "measgd" in args.method or "msgd" in args.method else 1.0)
+    hy = HyperParams(eta=eta, rho=wl["rho"], mu=0.9)
     cfg = make_config(args.method, workers=args.workers, iterations=args.iterations, batch_size=args.batch,
                       hyper=hy, seed=3)
     run_trainer(make_config(args.method, workers=args.workers, iterations=args.workers * 2,
