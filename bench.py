@@ -38,6 +38,28 @@ WORKLOADS = {
 }
 
 
+METRIC = "Sync EASGD samples/s (elastic-averaging round, 1 worker per B200)"
+CONFIG_NAME = {"lenet": "configs[1]: Sync EASGD, LeNet synthetic MNIST, 1 worker per GPU",
+               "cifar-quick": "Sync EASGD, CIFAR-quick synthetic CIFAR-10, 1 worker per GPU",
+               "alexnet": "configs[4]: Sync EASGD, AlexNet synthetic ImageNet 224x224, weak scaling"}
+
+
+def workload_config(args, b: int, world: int) -> dict:
+    return {"workload": f"{CONFIG_NAME[args.model]} (sync-easgd3, b={b}/worker)", "model": args.model,
+            "global_batch": world * b, "per_worker_batch": b, "parallelism": f"dp{world}",
+            "l2": "update kernel timed with L2 flushed; step inputs resident"}
+
+
+def traffic(kernel: str, model: str):
+    """Per-launch DRAM bytes (read + write) of a roofline kernel from the
+    committed ncu --set full capture summary (profiles/traffic.json)."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t.get(f"{kernel}:{model}", t.get(kernel))
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -205,10 +227,12 @@ def run_device(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ -> the step's launch list
         t0.record()
         for _ in range(args.steps):
             eng.step()
         t1.record()
+        torch.cuda.nvtx.range_pop()
         t1.synchronize()
         if world > 1:
             dist.barrier()
@@ -227,7 +251,7 @@ def run_device(args):
     src = "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback (B200_PROFILING.md)"
     roof_upd = {"kernel": "esgd_sync_update_f32 (k_sync_update<4>)", "bound": "hbm",
                 "achieved": round(upd_bytes / upd_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": None,
+                "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": traffic("sync_update", args.model),
                 "algorithmic_bytes_per_launch": upd_bytes, "launch_s": upd_s,
                 "peak_source": f"{src} hbm_gbs (copy)"}
     # dominant kernel of the step: the largest tcgen05 3xTF32 GEMM launch,
@@ -240,7 +264,7 @@ def run_device(args):
         ach = prec * fl / t / 1e12
         roof = {"kernel": f"esgd_tc_gemm_f32 (k_tc_gemm, {desc})", "bound": "tensor",
                 "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                "frac": round(ach / tf32_peak, 4), "traffic": None,
+                "frac": round(ach / tf32_peak, 4), "traffic": traffic("tc_gemm_dominant", args.model),
                 "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
                 "algorithmic_flops_per_launch": fl,
                 "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)"}
@@ -254,15 +278,12 @@ def run_device(args):
     comm_frac = bd["peer_param"] / dt if dt > 0 else 0.0
     cpu = cpu_baseline(args, spec, train) if (rank == 0 and world == 1 and not args.no_cpu) else None
     out = {
-        "metric": "Sync EASGD samples/s (elastic-averaging round, 1 worker per B200)",
+        "metric": METRIC,
         "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs)",
         "data": "synthetic (gen_synthetic blobs, HBM-resident)",
-        "config": {"workload": f"sync-easgd3 {args.model} b={b}/worker P={P}", "model": args.model,
-                   "global_batch": P * b, "params": eng.n, "parallelism": f"dp{world}",
-                   "l2": "update kernel timed with L2 flushed; step inputs resident",
-                   "graph": eng.graph is not None},
+        "config": dict(workload_config(args, b, world), params=eng.n, graph=eng.graph is not None),
         "roofline": roof,
         "roofline_update": roof_upd,
         "comm_fraction_exposed": round(comm_frac, 4),
@@ -430,45 +451,65 @@ class HostStager:
         return float(self.loss.numpy().mean())
 
 
+# CPU sample batch per worker round: AlexNet's b=128 round is ~10 s of numpy,
+# so the bounded sample uses a smaller batch (samples/s is per-sample work).
+CPU_SAMPLE_B = {"lenet": 64, "cifar-quick": 64, "alexnet": 16}
+
+
+class CpuRound:
+    """The CPU oracle (numpy restatement of the reference's sync round,
+    trainers/synchronous.py:57-64, P=1) on this host's cores."""
+
+    def __init__(self, args, train):
+        from oracle import esgd_oracle as O
+
+        self.O = O
+        layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK, "alexnet": O.alexnet_layers(1000)}[args.model]
+        self.wl = WORKLOADS[args.model]
+        self.b = min(args.batch or self.wl["b"], CPU_SAMPLE_B[args.model])
+        self.model = args.model
+        self.prob = O.NetProblem(*layers, train.samples, train.labels, seed=0, dtype=np.float32)
+        self.rng = O.worker_rng(3, 0)
+        self.w = self.prob.init_weights()
+        self.c = self.w.copy()
+        self.cores = int(os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+                         or os.cpu_count())
+        self.round()  # warm-up (BLAS init, page faults)
+
+    def round(self):
+        O, wl = self.O, self.wl
+        g = self.prob.gradient(self.w, self.rng, self.b)
+        s = O.tree_sum([self.w])
+        self.w, self.c = (O.easgd_worker_step(self.w, g, self.c, wl["eta"], wl["rho"]),
+                          O.easgd_center_step_from_sum(self.c, s, 1, wl["eta"], wl["rho"]))
+
+    def sample(self, budget_s: float):
+        """As many rounds as fit in ~budget_s (at least one): (rounds, seconds)."""
+        rounds, t0 = 0, time.perf_counter()
+        while True:
+            self.round()
+            rounds += 1
+            elapsed = time.perf_counter() - t0
+            if elapsed >= budget_s:
+                return rounds, elapsed
+
+    def describe(self, rounds: int) -> str:
+        return (f"{rounds} sync-easgd rounds of {self.model}, P=1, b={self.b}/round, numpy/OpenBLAS fp32 "
+                f"(oracle/esgd_oracle.py restating trainers/synchronous.py:57-64)")
+
+
 def cpu_baseline(args, spec, train, budget_s: float = 12.0):
-    """The CPU oracle (numpy restatement of the reference's sync round with
-    the same model) on this host, bounded sample: as many rounds as fit in
-    ~budget_s after one warm-up round."""
-    from oracle import esgd_oracle as O
-
-    layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK, "alexnet": O.alexnet_layers(1000)}[args.model]
-    wl = WORKLOADS[args.model]
-    b = args.batch or wl["b"]
-    prob = O.NetProblem(*layers, train.samples, train.labels, seed=0, dtype=np.float32)
-    rng = O.worker_rng(3, 0)
-    w = prob.init_weights()
-    c = w.copy()
-
-    def one_round(w, c):
-        g = prob.gradient(w, rng, b)
-        s = O.tree_sum([w])
-        return (O.easgd_worker_step(w, g, c, wl["eta"], wl["rho"]),
-                O.easgd_center_step_from_sum(c, s, 1, wl["eta"], wl["rho"]))
-
-    w, c = one_round(w, c)  # warm-up (BLAS init, page faults)
-    rounds = 1
-    t0 = time.perf_counter()
-    while True:
-        w, c = one_round(w, c)
-        rounds += 1
-        elapsed = time.perf_counter() - t0
-        if elapsed > budget_s:
-            break
-    timed = rounds - 1
-    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS") or str(os.cpu_count())
-    return {"value": round(timed * b / elapsed, 2) if timed > 0 else None, "unit": "samples/s",
-            "cores": int(threads), "kind": "port",
-            "sample": f"{timed} sync-easgd rounds of {args.model}, P=1, b={b}, numpy/OpenBLAS fp32 "
-                      f"(oracle/esgd_oracle.py restating trainers/synchronous.py:57-64)"}
+    cpu = CpuRound(args, train)
+    rounds, elapsed = cpu.sample(budget_s)
+    return {"value": round(rounds * cpu.b / elapsed, 2), "unit": "samples/s", "cores": cpu.cores,
+            "kind": "port", "sample": cpu.describe(rounds)}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the host."""
+    """--impl reference: the reference's CPU algorithm (the oracle port — the
+    reference is pure Python/numpy and is not installed on the GPU box) on the
+    host's cores, same metric/config as the native arm. Each step is a bounded
+    sample (>= 1 round, ~1 s) so the whole run stays within a few minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -478,20 +519,21 @@ def run_reference(args):
     train, _ = make_data(args.model, spec)
     wl = WORKLOADS[args.model]
     b = args.batch or wl["b"]
-    per_step_budget = 60.0 / max(1, args.steps + args.warmup)
-    vals = []
+    cpu = CpuRound(args, train)
+    per_step = min(2.0, 120.0 / max(1, args.steps + args.warmup))
+    tot_r, tot_t = 0, 0.0
     for i in range(args.steps + args.warmup):
-        r = cpu_baseline(args, spec, train, budget_s=min(10.0, per_step_budget))
-        if i >= args.warmup and r["value"]:
-            vals.append(r["value"])
-    value = float(np.mean(vals)) if vals else None
-    out = {"impl": "reference", "metric": "Sync EASGD samples/s (elastic-averaging round, 1 worker per B200)",
+        r, t = cpu.sample(per_step)
+        if i >= args.warmup:
+            tot_r, tot_t = tot_r + r, tot_t + t
+    value = round(tot_r * cpu.b / tot_t, 2)
+    out = {"impl": "reference", "metric": METRIC,
            "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1000.0 * tot_t / max(1, args.steps), 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic", "config": {"workload": f"sync-easgd {args.model} b={b}/worker P=1",
-                                           "model": args.model},
-           "cpu_baseline": {"value": value, "unit": "samples/s", "cores": r["cores"], "kind": "port",
-                            "sample": r["sample"]},
+           "data": "synthetic", "config": workload_config(args, b, 1),
+           "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cpu.cores, "kind": "port",
+                            "sample": cpu.describe(tot_r)},
            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -502,7 +544,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--model", default="lenet", choices=sorted(WORKLOADS))
+    ap.add_argument("--model", default="alexnet", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -1,0 +1,56 @@
+"""Small, deterministic launch sequences for ncu captures (profiles/).
+
+    python tools/ncu_case.py update     # fused elastic update on 61.1M params (AlexNet size), 5 launches
+    python tools/ncu_case.py dgrad      # tcgen05 conv2 dgrad GEMM (M=93312 N=1600 K=192), 4 launches
+    python tools/ncu_case.py wgrad      # tcgen05 conv2 wgrad GEMM (M=192 N=1600 K=93312), 4 launches
+"""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_1708_02983_b200 import HyperParams, _lib  # noqa: E402
+from paper_1708_02983_b200.device import stream_ptr  # noqa: E402
+from paper_1708_02983_b200.updates import sync_update_  # noqa: E402
+
+
+def update():
+    n = 61_100_840
+    ld = (n + 63) // 64 * 64
+    W = torch.randn((1, ld), device="cuda")
+    G = torch.randn_like(W)
+    Cc = torch.randn(ld, device="cuda")
+    S = torch.randn(ld, device="cuda")
+    hy = HyperParams(eta=0.01, rho=0.1)
+    for _ in range(5):
+        sync_update_(W, G, Cc, S, n, 8, hy)
+    torch.cuda.synchronize()
+
+
+def gemm(m, n, k, am, bm, cm):
+    kp, mp, np_ = (k + 3) // 4 * 4, (m + 3) // 4 * 4, (n + 3) // 4 * 4
+    A = torch.randn(kp * mp, device="cuda")
+    B = torch.randn(kp * np_, device="cuda")
+    Cm = torch.empty(mp * np_, device="cuda")
+    ws = torch.zeros(1 << 24, device="cuda")
+    c_sm, c_sn = (1, mp) if cm else (np_, 1)
+    d = _lib.TcGemmDesc(m, n, k, 1, A.data_ptr(), mp if am else kp, 0, B.data_ptr(), np_ if bm else kp, 0,
+                        Cm.data_ptr(), c_sm, c_sn, 0, None, 0, None, 0, 0, 0, 0, 0, 3, am, bm,
+                        ws.data_ptr(), ws.numel())
+    for _ in range(4):
+        _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    torch.cuda.set_device(0)
+    case = sys.argv[1]
+    if case == "update":
+        update()
+    elif case == "dgrad":
+        gemm(93312, 1600, 192, 1, 0, 1)
+    elif case == "wgrad":
+        gemm(192, 1600, 93312, 0, 0, 0)
+    print("ok", case)

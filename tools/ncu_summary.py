@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv   # per-kernel share of a step
     python tools/ncu_summary.py report gpurun_out/prof.ncu-rep      # key metrics of a --set full capture
+    python tools/ncu_summary.py report gpurun_out/prof_raw.csv      # same, from `ncu -i ... --page raw --csv`
 """
 import collections
 import csv
@@ -17,6 +18,12 @@ KEYS = [
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct",
+    "smsp__warps_issue_stalled_barrier_per_warp_active.pct",
+    "smsp__warps_issue_stalled_membar_per_warp_active.pct",
     "launch__registers_per_thread",
     "launch__grid_size",
     "launch__block_size",
@@ -38,7 +45,7 @@ def launches(path):
             continue
         v = float(d["Metric Value"])
         unit = d["Metric Unit"]
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         name = d["Kernel Name"].split("(")[0][:80]
         agg[name][0] += 1
         agg[name][1] += v
@@ -51,10 +58,16 @@ def launches(path):
 
 
 def report(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` output, converted on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
-    idx = {h: i for i, h in enumerate(hdr)}
+    idx = {}
+    for i, h in enumerate(hdr):  # raw-page names may carry a section prefix
+        idx.setdefault(h, i)
+        idx.setdefault(h.split(".", 2)[-1] if h.count(".") >= 3 and h.split(".")[0].isupper() else h, i)
     for r in rows[2:]:
         print(f"### {r[idx['Kernel Name']][:100]}")
         for k in KEYS:
