@@ -117,12 +117,62 @@ __global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64
   float* cz = col + z * col_sb + pix;
   const int k0 = blockIdx.y * grp, k1 = min(kdim, k0 + grp);
   int ci = k0 / khw, r = k0 - ci * khw, ky = r / kw, kx = r - ky * kw;
-  for (int k = k0; k < k1; ++k) {
-    const int iy = iy0 + ky, ix = ix0 + kx;
-    float v = 0.f;
-    if (iy >= 0 && iy < xd.h && ix >= 0 && ix < xd.w) v = __ldg(xz + ci * xd.sc + iy * xd.sh + ix * xd.sw);
-    cz[k * col_sk] = v;
-    if (++kx == kw) { kx = 0; if (++ky == kh) { ky = 0; ++ci; } }
+  // all of the group's loads first (independent, up to kGroup in flight per
+  // thread: the loop is latency-bound otherwise), then the coalesced stores
+  float v[kGroup];
+#pragma unroll
+  for (int t = 0; t < kGroup; ++t) {
+    v[t] = 0.f;
+    if (k0 + t < k1) {
+      const int iy = iy0 + ky, ix = ix0 + kx;
+      if (iy >= 0 && iy < xd.h && ix >= 0 && ix < xd.w) v[t] = __ldg(xz + ci * xd.sc + iy * xd.sh + ix * xd.sw);
+      if (++kx == kw) { kx = 0; if (++ky == kh) { ky = 0; ++ci; } }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kGroup; ++t)
+    if (k0 + t < k1) cz[(int64_t)(k0 + t) * col_sk] = v[t];
+}
+
+// transposed im2col for square KS x KS kernels over a unit-column-stride
+// input (the engine's CNHW planes): thread <-> output pixel, a group of
+// channels from blockIdx.y. Tap validity is two per-thread bit masks and the
+// input/output pointers just advance, so an element costs one predicated load
+// and one coalesced store (the generic kernel spent ~60 instructions on
+// address math per element and was issue-bound at ~1.8 TB/s).
+template <int KS>
+__global__ void __launch_bounds__(256) k_im2col_sq(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
+                                                   const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
+                                                   int stride, int pad, int oh, int ow, int cgrp) {
+  const int z = blockIdx.z;
+  const int ohw = oh * ow, np = xd.n * ohw;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= np) return;
+  const int img = pix / ohw, p = pix - img * ohw, oy = p / ow, ox = p - oy * ow;
+  const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
+  uint32_t rowok = 0, colok = 0;
+#pragma unroll
+  for (int t = 0; t < KS; ++t) {
+    rowok |= (uint32_t)(iy0 + t >= 0 && iy0 + t < xd.h) << t;
+    colok |= (uint32_t)(ix0 + t >= 0 && ix0 + t < xd.w) << t;
+  }
+  const int c0 = blockIdx.y * cgrp, c1 = min(xd.c, c0 + cgrp);
+  // (iy0, ix0) may lie in the padding: only valid taps are dereferenced
+  const float* xp = x + z * x_sb + img * xd.sn + (int64_t)c0 * xd.sc + (int64_t)iy0 * xd.sh + ix0;
+  float* cp = col + z * col_sb + (int64_t)c0 * KS * KS * col_sk + pix;
+  for (int c = c0; c < c1; ++c, xp += xd.sc) {
+#pragma unroll
+    for (int ky = 0; ky < KS; ++ky) {
+      const float* rp = xp + (int64_t)ky * xd.sh;
+      const bool rok = (rowok >> ky) & 1u;
+#pragma unroll
+      for (int kx = 0; kx < KS; ++kx) {
+        float v = 0.f;
+        if (rok && ((colok >> kx) & 1u)) v = __ldg(rp + kx);
+        *cp = v;
+        cp += col_sk;
+      }
+    }
   }
 }
 
@@ -156,6 +206,47 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
         acc += __ldg(dc + (int64_t)(ky * kw + kx) * col_sk + oy * ow + ox);
       }
     }
+    const int64_t o = img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
+    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    dx[z * x_sb + o] = acc;
+  }
+}
+
+// col2im for square KS x KS stride-1 kernels (AlexNet conv2-5, LeNet): the
+// KS*KS loads of a channel are issued together (predicated), then summed in
+// the same (ky, kx) order as k_col2im_t, so results are identical
+template <int KS>
+__global__ void __launch_bounds__(256) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+                                                   const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
+                                                   int pad, int oh, int ow, const float* __restrict__ mask,
+                                                   int64_t mask_sb, int grp) {
+  const int z = blockIdx.z;
+  const int hw = xd.h * xd.w, npin = xd.n * hw;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= npin) return;
+  const int img = q / hw, p = q - img * hw, yh = p / xd.w, xw = p - yh * xd.w;
+  const float* dz = dcol + z * col_sb + (int64_t)img * oh * ow;
+  // tap validity and pixel offsets are per-thread constants
+  int off[KS * KS];
+  bool ok[KS * KS];
+#pragma unroll
+  for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < KS; ++kx) {
+      const int oy = yh + pad - ky, ox = xw + pad - kx;
+      ok[ky * KS + kx] = oy >= 0 && oy < oh && ox >= 0 && ox < ow;
+      off[ky * KS + kx] = oy * ow + ox;
+    }
+  const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
+  for (int ci = c0; ci < c1; ++ci) {
+    const float* dc = dz + (int64_t)(ci * KS * KS) * col_sk;
+    float v[KS * KS];
+#pragma unroll
+    for (int t = 0; t < KS * KS; ++t) v[t] = ok[t] ? __ldg(dc + (int64_t)t * col_sk + off[t]) : 0.f;
+    float acc = 0.f;
+#pragma unroll
+    for (int t = 0; t < KS * KS; ++t)
+      if (ok[t]) acc += v[t];
     const int64_t o = img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
     if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
     dx[z * x_sb + o] = acc;
@@ -213,6 +304,35 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
   int ox_hi = (ix + pad) / stride;
   if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
   const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
+  if (oy_hi - oy_lo < 2 && ox_hi - ox_lo < 2) {
+    // <= 2x2 windows cover this pixel (k <= 2*stride, AlexNet 3/2, LeNet 2/2):
+    // issue the four argmax/dy loads together, sum in (oy, ox) order
+    const bool v01 = ox_lo + 1 <= ox_hi, v10 = oy_lo + 1 <= oy_hi;
+    const bool ok[4] = {oy_lo <= oy_hi && ox_lo <= ox_hi, oy_lo <= oy_hi && v01, v10 && ox_lo <= ox_hi, v10 && v01};
+    const int wo[4] = {oy_lo * yd.w + ox_lo, oy_lo * yd.w + ox_lo + 1, (oy_lo + 1) * yd.w + ox_lo,
+                       (oy_lo + 1) * yd.w + ox_lo + 1};
+    const int yo[4] = {oy_lo * yd.sh + ox_lo * yd.sw, oy_lo * yd.sh + (ox_lo + 1) * yd.sw,
+                       (oy_lo + 1) * yd.sh + ox_lo * yd.sw, (oy_lo + 1) * yd.sh + (ox_lo + 1) * yd.sw};
+    for (int c = c0; c < c1; ++c) {
+      const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
+      const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
+      int a[4];
+      float d[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[t] = ok[t] ? __ldg(ap + wo[t]) : -1;
+        d[t] = ok[t] ? __ldg(dyp + yo[t]) : 0.f;
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (a[t] == p) acc += d[t];
+      const int64_t o = img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
+      if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+      dx[z * x_sb + o] = acc;
+    }
+    return;
+  }
   for (int c = c0; c < c1; ++c) {
     const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
     const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
@@ -368,6 +488,17 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
                "im2col: col strides must be (>=K, 1) or (1, >=pixels)");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "im2col: batch > 65535");
   ESGD_REQUIRE(col && x, ESGD_ERR_INPUT, "im2col: null buffer");
+  if (col_sp == 1 && kh == kw && (kh == 3 || kh == 5 || kh == 11) && xd.sw == 1) {
+    const int gc = pick_group(np * batch * kh * kw / kGroup, xd.c);
+    dim3 g2((unsigned)((np + 255) / 256), (unsigned)((xd.c + gc - 1) / gc), batch);
+    if (kh == 3)
+      k_im2col_sq<3><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
+    else if (kh == 5)
+      k_im2col_sq<5><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
+    else
+      k_im2col_sq<11><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
+    return check_launch("esgd_im2col_f32");
+  }
   const int gi = pick_group(np * batch, kdim);
   if (col_sp == 1 && (kdim + gi - 1) / gi <= 65535) {
     dim3 g2((unsigned)((np + 255) / 256), (unsigned)((kdim + gi - 1) / gi), batch);
@@ -399,7 +530,11 @@ extern "C" int esgd_col2im_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const f
   if (col_sp == 1 && (xd.c + gc - 1) / gc <= 65535) {
     dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gc - 1) / gc), batch);
     dim3 b2(256);
-    if (stride == 1)
+    if (stride == 1 && kh == kw && kh == 3)
+      k_col2im_sq<3><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, pad, oh, ow, mask, mask_sb, gc);
+    else if (stride == 1 && kh == kw && kh == 5)
+      k_col2im_sq<5><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, pad, oh, ow, mask, mask_sb, gc);
+    else if (stride == 1)
       k_col2im_t<true><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb, gc);
     else
       k_col2im_t<false><<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dcol, col_sk, col_sb, kh, kw, stride, pad, oh, ow, mask, mask_sb, gc);

@@ -270,7 +270,10 @@ __device__ __forceinline__ void split_tile(uint32_t raw, uint32_t lo, int tid) {
       h.x = tf32_hi(x[j].x); h.y = tf32_hi(x[j].y); h.z = tf32_hi(x[j].z); h.w = tf32_hi(x[j].w);
       l.x = __fsub_rn(x[j].x, h.x); l.y = __fsub_rn(x[j].y, h.y);
       l.z = __fsub_rn(x[j].z, h.z); l.w = __fsub_rn(x[j].w, h.w);
-      sts4(raw + off, h);
+      // the hi part is NOT written back: kind::tf32 MMAs ignore the low 13
+      // mantissa bits of an fp32 operand (measured bit-exact against
+      // pre-truncated operands, tools/probe_tf32.py), so the raw tile already
+      // is B_hi to the tensor core — one 16 KB smem write less per k-block
       sts4(lo + off, l);
     }
   }

@@ -3,6 +3,9 @@
     python tools/ncu_case.py update     # fused elastic update on 61.1M params (AlexNet size), 5 launches
     python tools/ncu_case.py dgrad      # tcgen05 conv2 dgrad GEMM (M=93312 N=1600 K=192), 4 launches
     python tools/ncu_case.py wgrad      # tcgen05 conv2 wgrad GEMM (M=192 N=1600 K=93312), 4 launches
+    python tools/ncu_case.py im2col     # AlexNet conv2 im2col (64x27x27 -> colT[1600][93312]), 4 launches
+    python tools/ncu_case.py im2col1    # AlexNet conv1 im2col (3x224x224, 11x11 s4 -> colT[363][387200])
+    python tools/ncu_case.py col2im     # AlexNet conv2 col2im (colT[1600][93312] -> 64x27x27), 4 launches
 """
 import ctypes as C
 import sys
@@ -44,6 +47,26 @@ def gemm(m, n, k, am, bm, cm):
     torch.cuda.synchronize()
 
 
+def im2col(c, h, k, stride, pad, back=False):
+    b = 128
+    oh = (h + 2 * pad - k) // stride + 1
+    npix = b * oh * oh
+    np4 = (npix + 3) // 4 * 4
+    kd = c * k * k
+    x = torch.randn(c * b * h * h, device="cuda")
+    col = torch.randn(kd * np4, device="cuda")
+    xd = _lib.cnhw(b, c, h, h, b * h * h)
+    lib = _lib.load()
+    for _ in range(4):
+        if back:
+            _lib.check(lib.esgd_col2im_f32(x.data_ptr(), xd, 0, col.data_ptr(), 1, np4, 0, k, k, stride, pad,
+                                           oh, oh, None, 0, 1, stream_ptr()))
+        else:
+            _lib.check(lib.esgd_im2col_f32(col.data_ptr(), 1, np4, 0, x.data_ptr(), xd, 0, k, k, stride, pad,
+                                           oh, oh, 1, stream_ptr()))
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     case = sys.argv[1]
@@ -53,4 +76,10 @@ if __name__ == "__main__":
         gemm(93312, 1600, 192, 1, 0, 1)
     elif case == "wgrad":
         gemm(192, 1600, 93312, 0, 0, 0)
+    elif case == "im2col":
+        im2col(64, 27, 5, 1, 2)
+    elif case == "im2col1":
+        im2col(3, 224, 11, 4, 2)
+    elif case == "col2im":
+        im2col(64, 27, 5, 1, 2, back=True)
     print("ok", case)
