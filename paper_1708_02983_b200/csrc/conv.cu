@@ -284,6 +284,129 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, es
   }
 }
 
+// K x K max pooling over unit-column-stride planes: tap masks once per
+// thread, the channel loop only walks pointers; K*K independent loads per
+// channel, compared in (ky, kx) order with the generic kernel's tie rule
+template <int K>
+__global__ void __launch_bounds__(256) k_maxpool_fwd_sq(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
+                                                        int32_t* __restrict__ amax, const float* __restrict__ x,
+                                                        esgd_tensor4 xd, int64_t x_sb, int stride, int pad, int grp) {
+  const int z = blockIdx.z;
+  const int ohw = yd.h * yd.w, np = yd.n * ohw;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= np) return;
+  const int img = q / ohw, p = q - img * ohw, oy = p / yd.w, ox = p - oy * yd.w;
+  const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
+  bool ok[K * K];
+  int idx[K * K];
+#pragma unroll
+  for (int ky = 0; ky < K; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < K; ++kx) {
+      ok[ky * K + kx] = iy0 + ky >= 0 && iy0 + ky < xd.h && ix0 + kx >= 0 && ix0 + kx < xd.w;
+      idx[ky * K + kx] = (iy0 + ky) * xd.w + ix0 + kx;
+    }
+  const int c0 = blockIdx.y * grp, c1 = min(yd.c, c0 + grp);
+  const float* xp = x + z * x_sb + img * xd.sn + (int64_t)c0 * xd.sc + (int64_t)iy0 * xd.sh + ix0;
+  float* yp = y + z * y_sb + img * yd.sn + (int64_t)c0 * yd.sc + oy * yd.sh + ox * yd.sw;
+  int32_t* ap = amax + z * ((int64_t)yd.n * yd.c * ohw) + ((int64_t)img * yd.c + c0) * ohw + p;
+#pragma unroll 2
+  for (int c = c0; c < c1; ++c) {
+    float v[K * K];
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) v[ky * K + kx] = ok[ky * K + kx] ? __ldg(xp + ky * xd.sh + kx) : 0.f;
+    float best = -INFINITY;
+    int bi = -1;
+#pragma unroll
+    for (int t = 0; t < K * K; ++t)
+      if (ok[t] && (bi < 0 || v[t] > best)) { best = v[t]; bi = idx[t]; }
+    *yp = best;
+    *ap = bi;
+    xp += xd.sc;
+    yp += yd.sc;
+    ap += ohw;
+  }
+}
+
+// max-pool backward for K x K / stride 2 / pad 0 (AlexNet 3/2, LeNet 2/2):
+// thread <-> a 2x2 block of input pixels (2a..2a+1, 2b..2b+1), whose covering
+// windows are outputs (a-1..a, b-1..b) for K = 3 and (a, b) for K = 2, so one
+// thread loads 4 argmax + 4 dy values per channel for 4 outputs (the per-pixel
+// gather loads 8 per pixel). Each pixel still sums its windows in (oy, ox)
+// order, so results equal k_maxpool_bwd_t's.
+template <int K>
+__global__ void __launch_bounds__(256) k_maxpool_bwd_s2(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
+                                                        const int32_t* __restrict__ amax,
+                                                        const float* __restrict__ mask, int64_t mask_sb, int grp) {
+  const int z = blockIdx.z;
+  const int bh = (xd.h + 1) / 2, bw = (xd.w + 1) / 2, nb = bh * bw, ohw = yd.h * yd.w;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= xd.n * nb) return;
+  const int img = q / nb, r = q - img * nb, a = r / bw, b = r - a * bw;
+  // window slots: 0 (a-1,b-1) 1 (a-1,b) 2 (a,b-1) 3 (a,b); K = 2 uses slot 3 only
+  bool wok[4];
+  int wo[4], yo[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int oy = a - 1 + (t >> 1), ox = b - 1 + (t & 1);
+    wok[t] = (K == 3 || t == 3) && oy >= 0 && oy < yd.h && ox >= 0 && ox < yd.w;
+    wo[t] = oy * yd.w + ox;
+    yo[t] = oy * yd.sh + ox * yd.sw;
+  }
+  const int iy0 = 2 * a, ix0 = 2 * b;
+  const bool pok[4] = {true, ix0 + 1 < xd.w, iy0 + 1 < xd.h, iy0 + 1 < xd.h && ix0 + 1 < xd.w};
+  const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
+  const int32_t* ap = amax + z * ((int64_t)yd.n * yd.c * ohw) + ((int64_t)img * yd.c + c0) * ohw;
+  const float* dyp = dy + z * y_sb + img * yd.sn + (int64_t)c0 * yd.sc;
+  const int64_t o0 = img * xd.sn + (int64_t)c0 * xd.sc + iy0 * xd.sh + ix0 * xd.sw;
+  float* dxp = dx + z * x_sb + o0;
+  const float* mp = mask ? mask + z * mask_sb + o0 : nullptr;
+  const int p00 = iy0 * xd.w + ix0;
+  for (int c = c0; c < c1; ++c) {
+    int am[4];
+    float d[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      am[t] = wok[t] ? __ldg(ap + wo[t]) : -1;
+      d[t] = wok[t] ? __ldg(dyp + yo[t]) : 0.f;
+    }
+    // pixel (dy, dx) of the block: covered by slots with (slot row >= dy... ):
+    // (0,0): 0,1,2,3  (0,1): 1,3  (1,0): 2,3  (1,1): 3   [K = 3]
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (K == 3) {
+      if (am[0] == p00) acc[0] += d[0];
+      if (am[1] == p00) acc[0] += d[1];
+      if (am[2] == p00) acc[0] += d[2];
+      if (am[3] == p00) acc[0] += d[3];
+      if (am[1] == p00 + 1) acc[1] += d[1];
+      if (am[3] == p00 + 1) acc[1] += d[3];
+      if (am[2] == p00 + xd.w) acc[2] += d[2];
+      if (am[3] == p00 + xd.w) acc[2] += d[3];
+      if (am[3] == p00 + xd.w + 1) acc[3] += d[3];
+    } else {
+      if (am[3] == p00) acc[0] += d[3];
+      if (am[3] == p00 + 1) acc[1] += d[3];
+      if (am[3] == p00 + xd.w) acc[2] += d[3];
+      if (am[3] == p00 + xd.w + 1) acc[3] += d[3];
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!pok[t]) continue;
+      const int64_t off = (t >> 1) * xd.sh + (t & 1) * xd.sw;
+      float v = acc[t];
+      if (mp) v = __fmul_rn(v, mp[off] > 0.f ? 1.f : 0.f);
+      dxp[off] = v;
+    }
+    ap += ohw;
+    dyp += yd.sc;
+    dxp += xd.sc;
+    if (mp) mp += xd.sc;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                        const int32_t* __restrict__ amax,
@@ -313,9 +436,13 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
                        (oy_lo + 1) * yd.w + ox_lo + 1};
     const int yo[4] = {oy_lo * yd.sh + ox_lo * yd.sw, oy_lo * yd.sh + (ox_lo + 1) * yd.sw,
                        (oy_lo + 1) * yd.sh + ox_lo * yd.sw, (oy_lo + 1) * yd.sh + (ox_lo + 1) * yd.sw};
+    const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c0) * ohw;
+    const float* dyp = dy + z * y_sb + img * yd.sn + (int64_t)c0 * yd.sc;
+    const int64_t o0 = z * x_sb + img * xd.sn + (int64_t)c0 * xd.sc + iy * xd.sh + ix * xd.sw;
+    float* dxp = dx + o0;
+    const float* mp = mask ? mask + z * mask_sb + (o0 - z * x_sb) : nullptr;
+#pragma unroll 2
     for (int c = c0; c < c1; ++c) {
-      const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
-      const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
       int a[4];
       float d[4];
 #pragma unroll
@@ -327,9 +454,14 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (a[t] == p) acc += d[t];
-      const int64_t o = img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
-      if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
-      dx[z * x_sb + o] = acc;
+      if (mp) {
+        acc = __fmul_rn(acc, *mp > 0.f ? 1.f : 0.f);
+        mp += xd.sc;
+      }
+      *dxp = acc;
+      ap += ohw;
+      dyp += yd.sc;
+      dxp += xd.sc;
     }
     return;
   }
@@ -585,7 +717,12 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
     const int gp = pick_group((int64_t)yd.n * yd.h * yd.w * batch, yd.c);
     dim3 g2((unsigned)(((int64_t)yd.n * yd.h * yd.w + 255) / 256), (unsigned)((yd.c + gp - 1) / gp), batch);
     dim3 b2(256);
-    k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad, gp);
+    if (xd.sw == 1 && k == 3)
+      k_maxpool_fwd_sq<3><<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, stride, pad, gp);
+    else if (xd.sw == 1 && k == 2)
+      k_maxpool_fwd_sq<2><<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, stride, pad, gp);
+    else
+      k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad, gp);
     return check_launch("esgd_maxpool_fwd_f32");
   }
   int64_t total = (int64_t)yd.n * yd.c * yd.h * yd.w;
@@ -603,6 +740,17 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
                ESGD_ERR_SHAPE, "maxpool_bwd: bad geometry");
   ESGD_REQUIRE(batch <= 65535, ESGD_ERR_UNSUPPORTED, "maxpool: batch > 65535");
   ESGD_REQUIRE(dx && dy && argmax, ESGD_ERR_INPUT, "maxpool_bwd: null buffer");
+  if (stride == 2 && pad == 0 && (k == 2 || k == 3) && (yd.h - 1) * 2 + k <= xd.h + 1 &&
+      (yd.w - 1) * 2 + k <= xd.w + 1) {
+    const int64_t nblk = (int64_t)xd.n * ((xd.h + 1) / 2) * ((xd.w + 1) / 2);
+    const int gp = pick_group(nblk * batch, xd.c);
+    dim3 g2((unsigned)((nblk + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);
+    if (k == 3)
+      k_maxpool_bwd_s2<3><<<g2, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, gp);
+    else
+      k_maxpool_bwd_s2<2><<<g2, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, gp);
+    return check_launch("esgd_maxpool_bwd_f32");
+  }
   {
     const int gp = pick_group((int64_t)xd.n * xd.h * xd.w * batch, xd.c);
     dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);

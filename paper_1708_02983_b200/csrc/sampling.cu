@@ -30,37 +30,52 @@ __global__ void k_randint(int64_t* out, uint64_t seed, uint64_t counter, int64_t
     out[i] = (int64_t)(draw(seed, counter, (uint64_t)i) % upper);
 }
 
-// One CTA per (sample, replica): draw the row index, copy the row (128-bit
-// when the row pitch allows), write the label. The last CTA of a replica to
+// One CTA per (sample, row chunk, replica): draw the row index, copy the
+// chunk (128-bit when the row pitch allows, kUnroll independent loads in
+// flight per thread), chunk 0 writes the label. The last CTA of a replica to
 // finish advances that replica's counter by b so the launch is replayable.
+constexpr int kSampleThreads = 256, kSampleUnroll = 4;
+constexpr int64_t kSampleChunk = kSampleThreads * kSampleUnroll;  // vectors per CTA
+
 template <int V>
-__global__ void __launch_bounds__(128) k_sample_batch(float* __restrict__ xo, int64_t ldx_rep,
-                                                      int32_t* __restrict__ yo, int64_t* idx_out,
-                                                      const float* __restrict__ X,
-                                                      const int32_t* __restrict__ labels,
-                                                      int64_t n, int64_t d, uint64_t* rng_state,
-                                                      int32_t* ticket, int b) {
-  const int i = blockIdx.x, r = blockIdx.y;
+__global__ void __launch_bounds__(kSampleThreads) k_sample_batch(float* __restrict__ xo, int64_t ldx_rep,
+                                                                 int32_t* __restrict__ yo, int64_t* idx_out,
+                                                                 const float* __restrict__ X,
+                                                                 const int32_t* __restrict__ labels,
+                                                                 int64_t n, int64_t d, uint64_t* rng_state,
+                                                                 int32_t* ticket, int b) {
+  const int i = blockIdx.x, r = blockIdx.z;
   const uint64_t seed = rng_state[2 * r], counter = rng_state[2 * r + 1];
   const int64_t row = (int64_t)(draw(seed, counter, (uint64_t)i) % (uint64_t)n);
-  const float* src = X + row * d;
-  float* dst = xo + r * ldx_rep + (int64_t)i * d;
+  const int64_t nv = d / V, v0 = blockIdx.y * kSampleChunk;
   if (V == 4) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int64_t j = threadIdx.x; j < d / 4; j += blockDim.x) d4[j] = __ldg(s4 + j);
+    const float4* s4 = reinterpret_cast<const float4*>(X + row * d);
+    float4* d4 = reinterpret_cast<float4*>(xo + r * ldx_rep + (int64_t)i * d);
+    float4 t[kSampleUnroll];
+#pragma unroll
+    for (int u = 0; u < kSampleUnroll; ++u) {
+      const int64_t j = v0 + u * kSampleThreads + threadIdx.x;
+      if (j < nv) t[u] = __ldg(s4 + j);
+    }
+#pragma unroll
+    for (int u = 0; u < kSampleUnroll; ++u) {
+      const int64_t j = v0 + u * kSampleThreads + threadIdx.x;
+      if (j < nv) d4[j] = t[u];
+    }
   } else {
-    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) dst[j] = __ldg(src + j);
+    const float* src = X + row * d;
+    float* dst = xo + r * ldx_rep + (int64_t)i * d;
+    for (int64_t j = v0 + threadIdx.x; j < min(nv, v0 + kSampleChunk); j += kSampleThreads) dst[j] = __ldg(src + j);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && blockIdx.y == 0) {
     yo[r * b + i] = labels[row];
     if (idx_out) idx_out[r * b + i] = row;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    int t = atomicAdd(ticket + r, 1);
-    if (t == b - 1) {  // every CTA of this replica has read the counter
+    const int t = atomicAdd(ticket + r, 1);
+    if (t == b * (int)gridDim.y - 1) {  // every CTA of this replica has read the counter
       rng_state[2 * r + 1] = counter + (uint64_t)b;
       ticket[r] = 0;
       __threadfence();
@@ -129,12 +144,15 @@ extern "C" int esgd_sample_batch_f32(float* x_out, int64_t ldx_rep, int32_t* y_o
   ESGD_REQUIRE(b <= 65535 * 64 && nrep <= 65535, ESGD_ERR_UNSUPPORTED, "sample_batch: grid too large");
   ESGD_REQUIRE(x_out && y_out && X && labels && rng_state && ticket, ESGD_ERR_INPUT,
                "sample_batch: null buffer");
-  dim3 grid(b, nrep);
   bool v4 = (d & 3) == 0 && aligned16(x_out) && aligned16(X) && (ldx_rep & 3) == 0;
+  const int64_t nchunk = ((v4 ? d / 4 : d) + kSampleChunk - 1) / kSampleChunk;
+  ESGD_REQUIRE(nchunk <= 65535 && (int64_t)b * nchunk < (int64_t(1) << 31), ESGD_ERR_UNSUPPORTED,
+               "sample_batch: rows too long");
+  dim3 grid(b, (unsigned)nchunk, nrep);
   if (v4)
-    k_sample_batch<4><<<grid, 128, 0, ESGD_STREAM(stream)>>>(x_out, ldx_rep, y_out, idx_out, X, labels, n, d, rng_state, ticket, b);
+    k_sample_batch<4><<<grid, kSampleThreads, 0, ESGD_STREAM(stream)>>>(x_out, ldx_rep, y_out, idx_out, X, labels, n, d, rng_state, ticket, b);
   else
-    k_sample_batch<1><<<grid, 128, 0, ESGD_STREAM(stream)>>>(x_out, ldx_rep, y_out, idx_out, X, labels, n, d, rng_state, ticket, b);
+    k_sample_batch<1><<<grid, kSampleThreads, 0, ESGD_STREAM(stream)>>>(x_out, ldx_rep, y_out, idx_out, X, labels, n, d, rng_state, ticket, b);
   return check_launch("esgd_sample_batch_f32");
 }
 

@@ -329,3 +329,78 @@ def test_tcgen05_gemm_tma_store_epilogue(m, n, k, c_mcontig):
     # padding outside the m x n window untouched
     if c_mcontig and mp > m:
         assert out[m] == -5.0
+
+
+def _cnhw(x, plane):
+    n, c, h, w = x.shape
+    out = np.zeros((c, plane), np.float32)
+    out[:, :n * h * w] = x.transpose(1, 0, 2, 3).reshape(c, -1)
+    return out
+
+
+def _from_cnhw(a, n, c, h, w):
+    return a[:, :n * h * w].reshape(c, n, h, w).transpose(1, 0, 2, 3)
+
+
+@pytest.mark.parametrize("k,p,h,w", [(3, 1, 13, 13), (5, 2, 27, 27), (3, 1, 8, 7), (5, 2, 9, 12), (11, 2, 35, 35)])
+def test_square_kernel_im2col_col2im_cnhw_batched(k, p, h, w):
+    """the square-kernel engine paths (stride-1 col2im, any-stride im2col) on
+    CNHW planes with two replicas (z strides), bit-exact vs the oracle"""
+    rng = np.random.default_rng(k * 100 + h + w)
+    n, c, reps = 3, 5, 2
+    s = 4 if k == 11 else 1
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    npix = n * oh * ow
+    np4 = (npix + 3) // 4 * 4
+    plane = (n * h * w + 3) // 4 * 4
+    K = c * k * k
+    xs = [rng.standard_normal((n, c, h, w)).astype(np.float32) for _ in range(reps)]
+    xd = dev(np.stack([_cnhw(x, plane) for x in xs]))
+    colT = torch.zeros((reps, K, np4), device="cuda")
+    _lib.call("esgd_im2col_f32", colT.data_ptr(), 1, np4, K * np4, xd.data_ptr(), _lib.cnhw(n, c, h, w, plane),
+              c * plane, k, k, s, p, oh, ow, reps, stream_ptr())
+    for z in range(reps):
+        ref, _, _ = O._im2col(xs[z], k, s, p)
+        assert np.array_equal(host(colT[z])[:, :npix].T, ref), z
+    if s != 1:
+        return
+    dcolT = np.zeros((reps, K, np4), np.float32)
+    dcolT[:, :, :npix] = rng.standard_normal((reps, K, npix))
+    masks = [rng.standard_normal((n, c, h, w)).astype(np.float32) for _ in range(reps)]
+    dd, md = dev(dcolT), dev(np.stack([_cnhw(m, plane) for m in masks]))
+    dx = torch.zeros((reps, c, plane), device="cuda")
+    _lib.call("esgd_col2im_f32", dx.data_ptr(), _lib.cnhw(n, c, h, w, plane), c * plane, dd.data_ptr(), 1, np4,
+              K * np4, k, k, s, p, oh, ow, md.data_ptr(), c * plane, reps, stream_ptr())
+    for z in range(reps):
+        exp = O._col2im(dcolT[z, :, :npix].T.copy(), (n, c, h, w), k, s, p, oh, ow)
+        exp = exp * (masks[z] > 0)
+        assert np.array_equal(_from_cnhw(host(dx[z]), n, c, h, w), exp), z
+
+
+@pytest.mark.parametrize("k,h,w", [(3, 55, 55), (3, 13, 13), (3, 14, 9), (2, 24, 24), (2, 7, 8), (3, 27, 28)])
+def test_stride2_maxpool_cnhw_batched(k, h, w):
+    """the stride-2 max-pool paths (AlexNet 3/2, LeNet 2/2) on CNHW planes,
+    two replicas, ties and the relu mask, bit-exact vs the oracle"""
+    rng = np.random.default_rng(k * 1000 + h * 10 + w)
+    n, c, reps, s = 2, 3, 2, 2
+    oh, ow = (h - k) // s + 1, (w - k) // s + 1
+    plane, oplane = (n * h * w + 3) // 4 * 4, (n * oh * ow + 3) // 4 * 4
+    xs = [rng.standard_normal((n, c, h, w)).astype(np.float32) for _ in range(reps)]
+    xs[0][0, 0, :5, :5] = 0.5  # ties: first max in scan order wins
+    xd = dev(np.stack([_cnhw(x, plane) for x in xs]))
+    y = torch.zeros((reps, c, oplane), device="cuda")
+    am = torch.zeros((reps, n, c, oh, ow), dtype=torch.int32, device="cuda")
+    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), _lib.cnhw(n, c, oh, ow, oplane), c * oplane, am.data_ptr(),
+              xd.data_ptr(), _lib.cnhw(n, c, h, w, plane), c * plane, k, s, 0, reps, stream_ptr())
+    dys = [rng.standard_normal((n, c, oh, ow)).astype(np.float32) for _ in range(reps)]
+    dyd = dev(np.stack([_cnhw(d, oplane) for d in dys]))
+    dx = torch.zeros((reps, c, plane), device="cuda")
+    _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), _lib.cnhw(n, c, h, w, plane), c * plane, dyd.data_ptr(),
+              _lib.cnhw(n, c, oh, ow, oplane), c * oplane, am.data_ptr(), xd.data_ptr(), c * plane, k, s, 0,
+              reps, stream_ptr())
+    for z in range(reps):
+        ey, ea = O._maxpool(xs[z], k, s, 0)
+        assert np.array_equal(_from_cnhw(host(y[z]), n, c, oh, ow), ey), z
+        assert np.array_equal(host(am[z]), ea), z
+        exp = O._maxpool_bwd(dys[z], ea, (n, c, h, w)) * (xs[z] > 0)
+        assert np.array_equal(_from_cnhw(host(dx[z]), n, c, h, w), exp), z

@@ -6,6 +6,7 @@
     python tools/ncu_case.py im2col     # AlexNet conv2 im2col (64x27x27 -> colT[1600][93312]), 4 launches
     python tools/ncu_case.py im2col1    # AlexNet conv1 im2col (3x224x224, 11x11 s4 -> colT[363][387200])
     python tools/ncu_case.py col2im     # AlexNet conv2 col2im (colT[1600][93312] -> 64x27x27), 4 launches
+    python tools/ncu_case.py poolbwd    # AlexNet pool1 backward (64x55x55 <- 64x27x27, 3/2), 4 launches
 """
 import ctypes as C
 import sys
@@ -67,6 +68,22 @@ def im2col(c, h, k, stride, pad, back=False):
     torch.cuda.synchronize()
 
 
+def poolbwd():
+    b, c, h = 128, 64, 55
+    oh = (h - 3) // 2 + 1
+    x = torch.randn(c * b * h * h, device="cuda")
+    y = torch.empty(c * b * oh * oh, device="cuda")
+    am = torch.empty(c * b * oh * oh, dtype=torch.int32, device="cuda")
+    xd, yd = _lib.cnhw(b, c, h, h, b * h * h), _lib.cnhw(b, c, oh, oh, b * oh * oh)
+    lib = _lib.load()
+    _lib.check(lib.esgd_maxpool_fwd_f32(y.data_ptr(), yd, 0, am.data_ptr(), x.data_ptr(), xd, 0, 3, 2, 0, 1,
+                                        stream_ptr()))
+    for _ in range(4):
+        _lib.check(lib.esgd_maxpool_bwd_f32(x.data_ptr(), xd, 0, y.data_ptr(), yd, 0, am.data_ptr(), None, 0,
+                                            3, 2, 0, 1, stream_ptr()))
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     case = sys.argv[1]
@@ -82,4 +99,6 @@ if __name__ == "__main__":
         im2col(3, 224, 11, 4, 2)
     elif case == "col2im":
         im2col(64, 27, 5, 1, 2, back=True)
+    elif case == "poolbwd":
+        poolbwd()
     print("ok", case)
