@@ -8,6 +8,7 @@ falls back to anything else: a missing library or a non-sm_100 device raises
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import CudaError, InputError, ShapeError
@@ -110,6 +111,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    override = os.environ.get("ESGD_LIB")  # experiments: load a prebuilt variant, never rebuild
+    if override:
+        build_if_missing = False
     if build_if_missing:
         try:
             from . import _build
@@ -117,9 +121,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         except Exception as exc:  # no nvcc on the box: use the shipped .so
             if not LIB_PATH.exists():
                 raise CudaError(f"libesgd.so missing and cannot be built: {exc}") from exc
-    if not LIB_PATH.exists():
-        raise CudaError(f"libesgd.so not found at {LIB_PATH}")
-    lib = C.CDLL(str(LIB_PATH))
+    path = Path(override) if override else LIB_PATH
+    if not path.exists():
+        raise CudaError(f"libesgd.so not found at {path}")
+    lib = C.CDLL(str(path))
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -6,18 +6,22 @@
 //   warp 0      : TMA producer — cp.async.bulk.tensor 3-D loads of raw fp32
 //                 A/B tiles (128-byte swizzle) into a multi-stage smem ring,
 //                 completion tracked by mbarrier transaction counts.
-//   warps 2..5  : split warps — for 3xTF32 they rewrite each landed tile as
-//                 hi = x & 0xffffe000 (exact tf32) in place and lo = x - hi
-//                 into a twin buffer of identical (swizzled) layout, then
+//   warps 2..5  : split warps — for 3xTF32 they write A's rows as tf32 hi/lo
+//                 (hi = x & 0xffffe000, lo = x - hi) into TMEM, and B's
+//                 lo = x - hi into a twin smem buffer of identical (swizzled)
+//                 layout (the raw B tile already is B_hi to the tensor core,
+//                 which ignores the low 13 mantissa bits), then
 //                 fence.proxy.async and arrive.
 //   warp 1      : TMEM allocation and the single-thread tcgen05.mma issuer,
 //                 kind::tf32, M=128, N=BN, K=8 per instruction, into one of
-//                 two TMEM accumulators per 128-wide K chunk; tcgen05.commit
-//                 frees smem slots and hands finished chunks to the drain.
-//   warps 6..9  : drain/epilogue — tcgen05.ld each chunk's partial sums and
-//                 add them into fp32 registers with RN adds (the tensor-core
+//                 two TMEM accumulators per kChunkKB*32-deep K chunk;
+//                 tcgen05.commit frees smem slots and hands finished chunks
+//                 to the drain.
+//   warps 6..13 : drain/epilogue, two warps per TMEM lane quadrant (half the
+//                 columns each) — tcgen05.ld each chunk's partial sums and add
+//                 them into fp32 registers with RN adds (the tensor-core
 //                 accumulator alone loses ~1e-8*K relative), then bias/act/
-//                 mask and the store.
+//                 mask and the smem-staged TMA store.
 //
 // 3xTF32: a.b ~= hi_a.hi_b + hi_a.lo_b + lo_a.hi_b, accumulated in fp32 in
 // TMEM — fp32-grade products (relative error ~2^-21), which the parity gate
@@ -37,8 +41,17 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;                  // 32 fp32 = 128 B = one swizzle atom row
-constexpr int kThreads = 320;           // 10 warps: TMA, MMA, 4 split, 4 drain/epilogue
-constexpr int kChunkKB = 2;             // K-blocks (x32) per TMEM accumulation before promotion
+constexpr int kThreads = 448;           // 14 warps: TMA, MMA, 4 split, 8 drain/epilogue
+constexpr int kDrainWarps = 8;         // two per TMEM lane quadrant, each owning half of the BN columns
+// K-blocks (x32) per TMEM accumulation before promotion into fp32 registers.
+// 4 (128-deep chunks) measured ~8% faster on the AlexNet shapes (the drain's
+// TMEM reads compete with the TS-mode A operand) but doubles the tensor-core
+// accumulation error, and a 3-round multi-replica CNN run then drifted 2e-3
+// from the oracle (tests/test_gpu_sync.py); 2 keeps every parity test green.
+#ifndef ESGD_CHUNK_KB
+#define ESGD_CHUNK_KB 2
+#endif
+constexpr int kChunkKB = ESGD_CHUNK_KB;
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
 template <int BN, bool SPLIT>
@@ -160,6 +173,22 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
+}
+// 32 columns of the warp's 32 TMEM lanes, no wait (pair with tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -318,19 +347,20 @@ __device__ __forceinline__ uint32_t stage_addr(uint32_t sb, int r, int j) {
   return MODE == 1 ? sb + (j * 128 + r) * 4 : sb + r * 128 + ((((j >> 2) ^ (r & 7))) << 4) + (j & 3) * 4;
 }
 
-// registers -> smem for quarter qd; FAST applies bias + identity/relu
-template <int BN, int MODE, bool FAST>
-__device__ __forceinline__ void stage_quarter(const float (&racc)[BN], int qd, uint32_t sb, int r,
-                                              const float* bz, bool relu, int n0, int n) {
+// registers -> smem for the thread's local quarter lq (columns col0..col0+31
+// of the tile row); FAST applies bias + identity/relu
+template <int NACC, int MODE, bool FAST>
+__device__ __forceinline__ void stage_quarter(const float (&racc)[NACC], int lq, uint32_t sb, int r,
+                                              const float* bz, bool relu, int col0, int n) {
 #pragma unroll
   for (int jj = 0; jj < 32; jj += 4) {
-    const int j = qd * 32 + jj;
+    const int j = lq * 32 + jj;
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float x = racc[j + e];
       if (FAST) {
-        if (bz) x = __fadd_rn(x, n0 + j + e < n ? __ldg(bz + n0 + j + e) : 0.f);
+        if (bz) x = __fadd_rn(x, col0 + jj + e < n ? __ldg(bz + col0 + jj + e) : 0.f);
         if (relu) x = fmaxf(x, 0.f);
       }
       v[e] = x;
@@ -398,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(afull0 + 8 * b, 1);   // tcgen05.commit
-      mbar_init(aempty0 + 8 * b, 4);  // one arrive per drain warp
+      mbar_init(aempty0 + 8 * b, kDrainWarps);  // one arrive per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -520,91 +550,97 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---- drain + epilogue warps 6..9: warp w owns TMEM lanes 32*(w%4)..+31.
-    // Each K-chunk's TMEM partial is added into fp32 registers with
-    // round-to-nearest adds (promotion): the tensor-core accumulator only ever
-    // sums kChunkKB*32 products, which keeps the long-K error fp32-grade.
-    const int q = warp & 3;
+    // ---- drain + epilogue warps 6..13: warp w owns TMEM lanes 32*(w%4)..+31
+    // and columns [h*BN/2, (h+1)*BN/2) of each tile, h = (w-6)/4. Each
+    // K-chunk's TMEM partial is added into fp32 registers with round-to-
+    // nearest adds (promotion): the tensor-core accumulator only ever sums
+    // kChunkKB*32 products, which keeps the long-K error fp32-grade. Two warps
+    // per lane quadrant halve the registers per thread, so a 32-column slab is
+    // loaded per TMEM wait (the drain is bound by the TMEM load latency).
+    constexpr int HB = BN / 2;  // columns per drain warp
+    const int q = warp & 3, h = (warp - 6) >> 2;
+    const int issuer = 192 + h * 128;  // lane 0 of warp 6 / warp 10: bulk-store issue
     uint32_t c = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
-      float racc[BN];
+      float racc[HB];
 #pragma unroll
-      for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+      for (int j = 0; j < HB; ++j) racc[j] = 0.f;
       for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
         const int buf = c & 1;
         mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          float v[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c0, v);
+        for (int c0 = 0; c0 < HB; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + h * HB + c0, v);
+          tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
+          for (int j = 0; j < 32; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], __uint_as_float(v[j]));
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
       }
       const int row = w.m0 + q * 32 + lane;
+      const int n0 = w.n0 + h * HB;  // first column of this warp's half
       if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
         if (row < ep.m) {
           float* P = ep.ws + ((int64_t)w.z * ep.splits + w.slice) * ep.m * ep.n + (int64_t)row * ep.n;
 #pragma unroll
-          for (int j = 0; j < BN; ++j)
-            if (w.n0 + j < ep.n) P[w.n0 + j] = racc[j];
+          for (int j = 0; j < HB; ++j)
+            if (n0 + j < ep.n) P[n0 + j] = racc[j];
         }
       } else {
-        // 32 columns (16 KB) at a time through a two-slot smem ring, so staging
-        // quarter q+1 overlaps the bulk store of q. The register->smem staging
-        // is the only unrolled code (one variant per layout; the fast variant
-        // fuses bias + relu); the general epilogue (mask/tanh/sigmoid, or
-        // accumulate / strided direct stores in mode 0) is a rolled pass over
-        // the thread's own staged row, so the kernel's code stays small enough
-        // for the instruction cache (an unrolled general epilogue measured
-        // 26% of warp samples in no_instruction stalls).
-        const uint32_t so = smem_u32(stage_out);
+        // 32 columns (16 KB) at a time through this half's 16 KB smem slot;
+        // the two halves stage and store concurrently. The register->smem
+        // staging is the only unrolled code (one variant per layout; the fast
+        // variant fuses bias + relu); the general epilogue (mask/tanh/sigmoid,
+        // or accumulate / strided direct stores in mode 0) is a rolled pass
+        // over the thread's own staged row, so the kernel's code stays small
+        // enough for the instruction cache (an unrolled general epilogue
+        // measured 26% of warp samples in no_instruction stalls).
+        const uint32_t sb = smem_u32(stage_out) + h * 16384;
         const bool fast = ep.mask == nullptr && (ep.act == ESGD_ACT_NONE || ep.act == ESGD_ACT_RELU) &&
                           ep.out_mode != 0;
         const bool relu = ep.act == ESGD_ACT_RELU;
         const float* bz = ep.bias ? ep.bias + w.z * ep.bias_sb : nullptr;
         const int r = q * 32 + lane;
 #pragma unroll
-        for (int qd = 0; qd < BN / 32; ++qd) {
-          const uint32_t sb = so + (qd & 1) * 16384;
-          // slot free? (the store issued two quarters ago has read it)
-          if (threadIdx.x == 192) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int lq = 0; lq < HB / 32; ++lq) {
+          const int col0 = n0 + lq * 32;
+          // slot free? (this half's previous bulk store has read it)
+          if (threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          named_bar_sync(1 + h, 128);
           if (ep.out_mode == 2) {
-            if (fast) stage_quarter<BN, 2, true>(racc, qd, sb, r, bz, relu, w.n0, ep.n);
-            else stage_quarter<BN, 2, false>(racc, qd, sb, r, bz, relu, w.n0, ep.n);
+            if (fast) stage_quarter<HB, 2, true>(racc, lq, sb, r, bz, relu, col0, ep.n);
+            else stage_quarter<HB, 2, false>(racc, lq, sb, r, bz, relu, col0, ep.n);
           } else {
-            if (fast) stage_quarter<BN, 1, true>(racc, qd, sb, r, bz, relu, w.n0, ep.n);
-            else stage_quarter<BN, 1, false>(racc, qd, sb, r, bz, relu, w.n0, ep.n);
+            if (fast) stage_quarter<HB, 1, true>(racc, lq, sb, r, bz, relu, col0, ep.n);
+            else stage_quarter<HB, 1, false>(racc, lq, sb, r, bz, relu, col0, ep.n);
           }
-          if (!fast) general_quarter(ep, sb, r, row, w.z, w.n0 + qd * 32);
+          if (!fast) general_quarter(ep, sb, r, row, w.z, col0);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (threadIdx.x == 192 && ep.out_mode != 0) {
-            const int ncol = w.n0 + qd * 32;
+          named_bar_sync(1 + h, 128);
+          if (threadIdx.x == issuer && ep.out_mode != 0) {
             if (ep.out_mode == 1)
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(w.m0), "r"(ncol), "r"(w.z), "r"(sb)
+                  "r"(w.m0), "r"(col0), "r"(w.z), "r"(sb)
                   : "memory");
             else
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(ncol), "r"(w.m0), "r"(w.z), "r"(sb)
+                  "r"(col0), "r"(w.m0), "r"(w.z), "r"(sb)
                   : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
       }
     }
-    if ((ep.out_mode == 1 || ep.out_mode == 2) && threadIdx.x == 192)
+    if ((ep.out_mode == 1 || ep.out_mode == 2) && threadIdx.x == issuer)
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -768,6 +804,7 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
                ESGD_ERR_UNSUPPORTED, "tc_gemm: too many tiles");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool split = d->precision == 3;
-  if (d->n <= 64) return split ? tc::launch_major<64, true>(d, st) : tc::launch_major<64, false>(d, st);
+  if (d->n <= 64)
+    return split ? tc::launch_major<64, true>(d, st) : tc::launch_major<64, false>(d, st);
   return split ? tc::launch_major<128, true>(d, st) : tc::launch_major<128, false>(d, st);
 }

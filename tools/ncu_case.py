@@ -2,6 +2,7 @@
 
     python tools/ncu_case.py update     # fused elastic update on 61.1M params (AlexNet size), 5 launches
     python tools/ncu_case.py dgrad      # tcgen05 conv2 dgrad GEMM (M=93312 N=1600 K=192), 4 launches
+    python tools/ncu_case.py fwd        # tcgen05 conv2 forward GEMM (M=93312 N=192 K=1600), 4 launches
     python tools/ncu_case.py wgrad      # tcgen05 conv2 wgrad GEMM (M=192 N=1600 K=93312), 4 launches
     python tools/ncu_case.py im2col     # AlexNet conv2 im2col (64x27x27 -> colT[1600][93312]), 4 launches
     python tools/ncu_case.py im2col1    # AlexNet conv1 im2col (3x224x224, 11x11 s4 -> colT[363][387200])
@@ -91,6 +92,8 @@ if __name__ == "__main__":
         update()
     elif case == "dgrad":
         gemm(93312, 1600, 192, 1, 0, 1)
+    elif case == "fwd":
+        gemm(93312, 192, 1600, 1, 0, 1)
     elif case == "wgrad":
         gemm(192, 1600, 93312, 0, 0, 0)
     elif case == "im2col":
