@@ -1,17 +1,18 @@
-# Round-1 ncu captures for profiles/ (run on the GPU box: gpurun -- bash tools/capture_profiles.sh).
-# Reports are converted to CSV/text on the box; only the small update .ncu-rep travels back.
+# Round ncu captures for profiles/ (run on the GPU box:
+#   gpurun -- bash tools/capture_profiles.sh
+# Reports are converted to CSV/text on the box (tools/ncu_capture.sh); only
+# small files travel back. Each program first runs once without ncu.
 set -x
-cap() { # name kernel-regex case
-  python tools/ncu_case.py $3 && ncu --set full --import-source on --clock-control none -k regex:$2 -s 2 -c 1 -o /tmp/$1 python tools/ncu_case.py $3 > gpurun_out/$1.log 2>&1
-  ncu -i /tmp/$1.ncu-rep --page raw --csv > gpurun_out/$1_raw.csv 2>&1
-  ncu -i /tmp/$1.ncu-rep --page details > gpurun_out/$1_details.txt 2>&1
-  ncu -i /tmp/$1.ncu-rep --page source --csv > gpurun_out/$1_source.csv 2>&1
-}
-cap r01_update k_sync_update update
-cap r01_tc_dgrad k_tc_gemm dgrad
-cap r01_tc_wgrad k_tc_gemm wgrad
-cp /tmp/r01_update.ncu-rep gpurun_out/
-python bench.py --model lenet --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain34.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r01_launches_lenet.csv python bench.py --model lenet --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu34d.log 2>&1
-python bench.py --model alexnet --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain34e.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r01_launches_alexnet.csv python bench.py --model alexnet --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu34e.log 2>&1
-du -sh gpurun_out; ls -la gpurun_out
-echo done
+bash tools/ncu_capture.sh r01_update k_sync_update update
+bash tools/ncu_capture.sh r01_tc_wgrad k_tc_gemm wgrad
+bash tools/ncu_capture.sh r01_tc_dgrad k_tc_gemm dgrad
+bash tools/ncu_capture.sh r01_tc_fwd k_tc_gemm fwd
+cp /tmp/r01_update.ncu-rep gpurun_out/ 2>/dev/null
+# launch lists of the timed region only (NVTX range "timed" in bench.py)
+for m in alexnet lenet; do
+  python bench.py --model $m --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain_$m.log 2>&1 &&
+  ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/r01_launches_$m.csv python bench.py --model $m --steps 3 --warmup 3 --no-e2e --no-cpu \
+      > gpurun_out/ncu_launch_$m.log 2>&1
+done
+ls -la gpurun_out
