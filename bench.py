@@ -138,14 +138,18 @@ def dist_setup(n_gpus: int):
 
 
 def time_update_kernel(eng, reps: int = 20):
-    """Live CUDA-event timing of the fused elastic update on the training
-    stream with the engine's own buffers (algorithmic bytes: 24 B/param at
-    nrep=1, 16 B per extra replica)."""
+    """Live CUDA-event timing of the round's elastic-update kernel on the
+    training stream with copies of the engine's buffers, L2 flushed before
+    each launch. Algorithmic bytes per param: C read+write and S read (12) +
+    12 per local replica (W read+write, G read) = 24 at nrep = 1, plus the
+    S_next write (4) when the update also forms the next round's replica sum
+    (esgd_sync_update_sum_f32, the engine's path without groups)."""
     import torch
 
-    from paper_1708_02983_b200.updates import sync_update_
+    from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_
 
     n, nrep = eng.n, eng.nrep
+    fused = getattr(eng, "fused_sum", False)
     # work on copies so the training state is untouched
     W, G, C, S = eng.W.clone(), eng.G.clone(), eng.C.clone(), eng.S.clone()
     flush = torch.empty(int(256e6) // 4, device=W.device)
@@ -154,13 +158,17 @@ def time_update_kernel(eng, reps: int = 20):
         flush.zero_()  # evict L2 (126 MB) so the stream comes from HBM
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        sync_update_(W, G, C, S, n, eng.P, eng.cfg.hyper)
+        if fused:
+            sync_update_sum_(W, G, C, S, S, n, eng.P, eng.cfg.hyper)
+        else:
+            sync_update_(W, G, C, S, n, eng.P, eng.cfg.hyper)
         b.record()
         b.synchronize()
         if i >= 3:
             times.append(a.elapsed_time(b) / 1e3)
-    bytes_ = n * (8 + 16 * nrep)
-    return bytes_, float(np.mean(times))
+    bytes_ = n * (12 + 12 * nrep + (4 if fused else 0))
+    name = "esgd_sync_update_sum_f32 (k_sync_update_sum4)" if fused else "esgd_sync_update_f32 (k_sync_update<4>)"
+    return bytes_, float(np.mean(times)), name, ("sync_update_sum" if fused else "sync_update")
 
 
 def time_dominant_gemm(eng, reps: int = 10):
@@ -245,13 +253,13 @@ def run_device(args):
     value = samples / dt
 
     # elastic-update kernel roofline (live, CUDA events, L2 flushed)
-    upd_bytes, upd_s = time_update_kernel(eng)
+    upd_bytes, upd_s, upd_name, upd_key = time_update_kernel(eng)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     src = "MEASURED_PEAKS.json" if not pk.get("_fallback") else "fallback (B200_PROFILING.md)"
-    roof_upd = {"kernel": "esgd_sync_update_f32 (k_sync_update<4>)", "bound": "hbm",
+    roof_upd = {"kernel": upd_name, "bound": "hbm",
                 "achieved": round(upd_bytes / upd_s / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": traffic("sync_update", args.model),
+                "frac": round(upd_bytes / upd_s / 1e9 / hbm, 4), "traffic": traffic(upd_key, args.model),
                 "algorithmic_bytes_per_launch": upd_bytes, "launch_s": upd_s,
                 "peak_source": f"{src} hbm_gbs (copy)"}
     # dominant kernel of the step: the largest tcgen05 3xTF32 GEMM launch,
@@ -315,9 +323,13 @@ def launches_per_step(eng) -> int:
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         eng.plan.gradient(G, W, stream_ptr())
         from paper_1708_02983_b200.fabric.collectives import replica_sum_
-        replica_sum_(eng.S.clone(), W, eng.n)
-        from paper_1708_02983_b200.updates import sync_update_
-        sync_update_(W, G, eng.C.clone(), eng.S.clone(), eng.n, eng.P, eng.cfg.hyper)
+        from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_
+        if getattr(eng, "fused_sum", False):
+            S = eng.S.clone()
+            sync_update_sum_(W, G, eng.C.clone(), S, S, eng.n, eng.P, eng.cfg.hyper)
+        else:
+            replica_sum_(eng.S.clone(), W, eng.n)
+            sync_update_(W, G, eng.C.clone(), eng.S.clone(), eng.n, eng.P, eng.cfg.hyper)
         torch.cuda.synchronize()
     n = 0
     for e in prof.events():
@@ -336,7 +348,8 @@ def run_e2e(args, spec, train, cfg, world):
 
     prob = NetworkProblem(spec, train, None)
     eng = SyncEngine(cfg, prob, use_graph=False, profile_rounds=0)
-    stager = HostStager(prob, eng)
+    # big rows: per-row DMA from the pinned dataset; small rows: host gather + one H2D
+    stager = DmaStager(prob, eng) if spec.input_dim * 4 >= 65536 else HostStager(prob, eng)
     for _ in range(max(1, args.warmup)):
         stager.step()
     torch.cuda.synchronize()
@@ -353,7 +366,9 @@ def run_e2e(args, spec, train, cfg, world):
     b = cfg.batch_size
     return {"value": round(args.steps * cfg.cluster.workers * b / dt, 1), "unit": "samples/s",
             "h2d_bytes_per_step": stager.h2d_bytes, "d2h_bytes_per_step": stager.d2h_bytes,
-            "path": "host SplitMix64 sampling + gather -> pinned batch -> (graph: H2D, round, loss D2H) -> sync"}
+            "path": ("host SplitMix64 sampling -> per-row DMA from the pinned dataset (copy stream, overlapped) -> "
+                     "(graph: round, loss D2H) -> sync" if isinstance(stager, DmaStager) else
+                     "host SplitMix64 sampling + gather -> pinned batch -> (graph: H2D, round, loss D2H) -> sync")}
 
 
 class HostStager:
@@ -447,6 +462,96 @@ class HostStager:
         self._graph(k).replay()                              # H2D + round + loss D2H (async)
         self.pending = self.pool.submit(self._stage_host, k ^ 1)  # stage the next batch meanwhile
         torch.cuda.current_stream().synchronize()
+        self.cur = k ^ 1
+        return float(self.loss.numpy().mean())
+
+
+class DmaStager(HostStager):
+    """Host data path for big rows (ImageNet-sized): the dataset lives in
+    pinned host memory; each round's rows are drawn on the host with the
+    workers' SplitMix64 streams and copied straight to one of two device
+    batch buffers by DMA (esgd_gather_rows_h2d: one cudaMemcpyAsync per row
+    on a copy stream — no host-side gather, no SMs), overlapped with the
+    previous round; one CUDA graph per buffer runs the round and the D2H of
+    the round's mean loss, which is read back after every round."""
+
+    def __init__(self, prob, eng):
+        import torch
+
+        from paper_1708_02983_b200.rng import CounterRng, stream_seed
+
+        self.prob, self.eng = prob, eng
+        net = eng.plan.net
+        self.net = net
+        b, nrep, d = net.b, net.nrep, net.d_in
+        X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
+        self.n, self.d = X.shape
+        self.Xp = torch.from_numpy(X).pin_memory()  # setup, outside the timed region
+        self.Y = prob.train.labels.astype(np.int32)
+        self.rngs = [CounterRng(stream_seed(eng.cfg.seed, w)) for w in range(eng.first, eng.first + nrep)]
+        self.xb = [torch.empty((nrep, b * d), dtype=torch.float32, device="cuda") for _ in range(2)]
+        self.yb = [torch.empty((nrep, b), dtype=torch.int32, device="cuda") for _ in range(2)]
+        self.hy = [torch.empty((nrep, b), dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
+        self.h2d_bytes = nrep * b * d * 4 + nrep * b * 4
+        self.d2h_bytes = nrep * 4
+        self.graphs = [None, None]
+        self.copy = torch.cuda.Stream()
+        self.ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self.x0, self.y0 = net.x, net.y
+        self.cur = 0
+        self._load(0)
+
+    def _load(self, k):
+        import torch
+
+        from paper_1708_02983_b200 import _lib
+        from paper_1708_02983_b200.device import stream_ptr
+
+        lib = _lib.load()
+        net, hy = self.net, self.hy[k].numpy()
+        for r, rng in enumerate(self.rngs):
+            idx = np.ascontiguousarray(rng.randint_block(net.b, self.n), dtype=np.int64)
+            hy[r] = self.Y[idx]
+            _lib.check(lib.esgd_gather_rows_h2d(self.xb[k][r].data_ptr(), self.d * 4, self.Xp.data_ptr(),
+                                                self.d * 4, idx.ctypes.data, net.b, self.d * 4, self.n,
+                                                stream_ptr(self.copy)), "gather_rows_h2d")
+        with torch.cuda.stream(self.copy):
+            self.yb[k].copy_(self.hy[k], non_blocking=True)
+        self.ev[k].record(self.copy)
+
+    def _device_round(self, k):
+        import torch
+
+        from paper_1708_02983_b200.device import stream_ptr
+
+        eng, net = self.eng, self.net
+        cs = torch.cuda.current_stream()
+        eng.comm.wait_stream(cs)
+        with torch.cuda.stream(eng.comm):
+            eng._sum(eng.comm)
+        net.gradient(eng.G, eng.W, stream_ptr(cs))
+        cs.wait_stream(eng.comm)
+        eng._update(cs)
+        self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
+
+    def _graph(self, k):
+        # the round of buffer k reads xb[k] / yb[k] directly (captured pointers)
+        self.net.x, self.net.y = self.xb[k], self.yb[k]
+        try:
+            return super()._graph(k)
+        finally:
+            self.net.x, self.net.y = self.x0, self.y0
+
+    def step(self):
+        import torch
+
+        k = self.cur
+        cs = torch.cuda.current_stream()
+        cs.wait_event(self.ev[k])      # batch k on the device
+        self._graph(k).replay()        # round + loss D2H (async)
+        self._load(k ^ 1)              # next batch by DMA, concurrent with round k
+        cs.synchronize()
         self.cur = k ^ 1
         return float(self.loss.numpy().mean())
 

@@ -64,6 +64,14 @@ int esgd_sync_update_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int
                          float* C, const float* S, int64_t n, float eta, float etarho,
                          int32_t num_workers, esgd_stream_t stream);
 
+/* esgd_sync_update_f32 plus the next round's local replica sum (the
+ * tree_sum of fabric/collectives.py:18-32 over the updated replicas, same
+ * binomial order): S_next = sum_r W_r(t+1). S_next may alias S. 1 <= nrep
+ * <= 8, 16-B aligned buffers/pitches. 28 B/param at nrep = 1.              */
+int esgd_sync_update_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
+                             float* C, const float* S, float* S_next, int64_t n, float eta,
+                             float etarho, int32_t num_workers, esgd_stream_t stream);
+
 /* measgd_worker_step, updates.py:134-140 (in place):
  *   v = mu*v - eta*g;  w = (w + v) - etarho*(w - c).  24 B/param.          */
 int esgd_measgd_update_f32(float* w, float* v, const float* g, const float* c, int64_t n,
@@ -114,6 +122,14 @@ int esgd_sample_batch_f32(float* x_out, int64_t ldx_rep, int32_t* y_out, int64_t
                           const float* X, const int32_t* labels, int64_t n, int64_t d,
                           uint64_t* rng_state, int32_t* ticket, int32_t b, int32_t nrep,
                           esgd_stream_t stream);
+
+/* Host data path (the e2e loader): copy rows[i] of a PINNED host matrix
+ * (src, row pitch src_pitch bytes, src_rows rows) to dst + i*dst_pitch on
+ * the device with DMA (cudaMemcpyAsync per row run, no SMs used, no host
+ * gather). rows: host array of nrows indices. Asynchronous on `stream`.    */
+int esgd_gather_rows_h2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                         const int64_t* rows, int32_t nrows, int64_t row_bytes, int64_t src_rows,
+                         esgd_stream_t stream);
 
 /* QuadraticProblem.gradient, trainers/problems.py:95-96:
  *   G[r] = curvature*(W[r] - target) for nrep replicas.                    */

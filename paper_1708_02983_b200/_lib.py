@@ -75,6 +75,7 @@ _SIGS = {
     "esgd_worker_step_f32": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, vp]),
     "esgd_center_step_from_sum_f32": (C.c_int, [vp, vp, vp, i64, f32, i32, vp]),
     "esgd_sync_update_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, f32, f32, i32, vp]),
+    "esgd_sync_update_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, vp, i64, f32, f32, i32, vp]),
     "esgd_measgd_update_f32": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, f32, vp]),
     "esgd_center_incr_f32": (C.c_int, [vp, vp, vp, i64, f32, vp]),
     "esgd_exchange_update_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
@@ -85,6 +86,7 @@ _SIGS = {
     "esgd_replica_tree_sum_f32": (C.c_int, [vp, vp, i64, i32, i64, vp]),
     "esgd_randint_u64": (C.c_int, [vp, u64, u64, i64, u64, vp]),
     "esgd_sample_batch_f32": (C.c_int, [vp, i64, vp, vp, vp, vp, i64, i64, vp, vp, i32, i32, vp]),
+    "esgd_gather_rows_h2d": (C.c_int, [vp, i64, vp, i64, vp, i32, i64, i64, vp]),
     "esgd_quadratic_grad_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, vp]),
     "esgd_gemm_f32": (C.c_int, [C.POINTER(GemmDesc), vp]),
     "esgd_tc_gemm_f32": (C.c_int, [C.POINTER(TcGemmDesc), vp]),

@@ -156,6 +156,30 @@ extern "C" int esgd_sample_batch_f32(float* x_out, int64_t ldx_rep, int32_t* y_o
   return check_launch("esgd_sample_batch_f32");
 }
 
+extern "C" int esgd_gather_rows_h2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                                    const int64_t* rows, int32_t nrows, int64_t row_bytes, int64_t src_rows,
+                                    esgd_stream_t stream) {
+  ESGD_REQUIRE(nrows >= 0 && row_bytes >= 0 && dst_pitch >= row_bytes && src_pitch >= row_bytes, ESGD_ERR_SHAPE,
+               "gather_rows_h2d: bad geometry");
+  if (nrows == 0 || row_bytes == 0) return ESGD_OK;
+  ESGD_REQUIRE(dst && src && rows, ESGD_ERR_INPUT, "gather_rows_h2d: null pointer");
+  cudaStream_t st = ESGD_STREAM(stream);
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  for (int32_t i = 0; i < nrows;) {
+    const int64_t r = rows[i];
+    ESGD_REQUIRE(r >= 0 && r < src_rows, ESGD_ERR_INPUT, "gather_rows_h2d: row %lld out of range [0, %lld)",
+                 (long long)r, (long long)src_rows);
+    int32_t run = 1;  // merge consecutive source rows into one transfer when the pitches allow
+    while (i + run < nrows && rows[i + run] == r + run && dst_pitch == src_pitch) ++run;
+    const cudaError_t e = cudaMemcpyAsync(d + (int64_t)i * dst_pitch, s + r * src_pitch,
+                                          (size_t)((run - 1) * src_pitch + row_bytes), cudaMemcpyHostToDevice, st);
+    ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "gather_rows_h2d: %s", cudaGetErrorString(e));
+    i += run;
+  }
+  return ESGD_OK;
+}
+
 extern "C" int esgd_quadratic_grad_f32(float* G, int64_t ldg, const float* W, int64_t ldw,
                                        int32_t nrep, const float* target, const float* curvature,
                                        int64_t n, esgd_stream_t stream) {

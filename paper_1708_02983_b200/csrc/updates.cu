@@ -378,6 +378,68 @@ extern "C" int esgd_worker_step_f32(float* w_out, const float* w, const float* g
   return check_launch("esgd_worker_step_f32");
 }
 
+// The round update of k_sync_update plus the NEXT round's local replica sum:
+// S_next = tree_sum(W_r(t+1)) in the reference's binomial order, from the
+// registers that hold the new replicas — the separate replica-sum pass
+// (8 B/param at P_local = 1) disappears. S_next may alias S (each element is
+// read before it is written, by the same thread). 28 B/param at nrep = 1.
+template <int MAXP>
+__global__ void __launch_bounds__(256) k_sync_update_sum4(float* W, int64_t ldw, const float* __restrict__ G,
+                                                          int64_t ldg, int nrep, float* C, const float* S,
+                                                          float* S_next, int64_t n, float eta, float er,
+                                                          float p) {
+  const int64_t nv = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 c = ld4rw(C + 4 * i), s = ld4rw(S + 4 * i);
+    float vx[MAXP], vy[MAXP], vz[MAXP], vw[MAXP];
+#pragma unroll
+    for (int r = 0; r < MAXP; ++r) {
+      if (r < nrep) {
+        float* wp = W + r * ldw + 4 * i;
+        const float4 w = ld4rw(wp), g = ld4(G + r * ldg + 4 * i);
+        float4 o;
+        o.x = worker_rule(w.x, g.x, c.x, eta, er);
+        o.y = worker_rule(w.y, g.y, c.y, eta, er);
+        o.z = worker_rule(w.z, g.z, c.z, eta, er);
+        o.w = worker_rule(w.w, g.w, c.w, eta, er);
+        st4(wp, o);
+        vx[r] = o.x; vy[r] = o.y; vz[r] = o.z; vw[r] = o.w;
+      } else {
+        vx[r] = vy[r] = vz[r] = vw[r] = 0.f;
+      }
+    }
+    float4 o;
+    o.x = center_rule(c.x, s.x, p, er);
+    o.y = center_rule(c.y, s.y, p, er);
+    o.z = center_rule(c.z, s.z, p, er);
+    o.w = center_rule(c.w, s.w, p, er);
+    st4(C + 4 * i, o);
+    float4 t;
+    t.x = binomial_sum<MAXP>(vx, nrep);
+    t.y = binomial_sum<MAXP>(vy, nrep);
+    t.z = binomial_sum<MAXP>(vz, nrep);
+    t.w = binomial_sum<MAXP>(vw, nrep);
+    st4(S_next + 4 * i, t);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t j = (n & ~int64_t(3)) + threadIdx.x;
+    const float c = C[j], s = S[j];
+    float v[MAXP];
+#pragma unroll
+    for (int r = 0; r < MAXP; ++r) {
+      if (r < nrep) {
+        float* wp = W + r * ldw + j;
+        *wp = v[r] = worker_rule(*wp, G[r * ldg + j], c, eta, er);
+      } else {
+        v[r] = 0.f;
+      }
+    }
+    C[j] = center_rule(c, s, p, er);
+    S_next[j] = binomial_sum<MAXP>(v, nrep);
+  }
+}
+
 extern "C" int esgd_center_step_from_sum_f32(float* c_out, const float* c, const float* s,
                                              int64_t n, float etarho, int32_t num_workers,
                                              esgd_stream_t stream) {
@@ -410,6 +472,29 @@ extern "C" int esgd_sync_update_f32(float* W, int64_t ldw, const float* G, int64
   else
     k_sync_update<1><<<stride_grid(n, 256), 256, 0, ESGD_STREAM(stream)>>>(W, ldw, G, ldg, nrep, C, S, n, eta, etarho, p);
   return check_launch("esgd_sync_update_f32");
+}
+
+extern "C" int esgd_sync_update_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg,
+                                        int32_t nrep, float* C, const float* S, float* S_next, int64_t n,
+                                        float eta, float etarho, int32_t num_workers, esgd_stream_t stream) {
+  ESGD_REQUIRE(n >= 0 && nrep >= 1, ESGD_ERR_SHAPE, "sync_update_sum: bad size");
+  ESGD_REQUIRE(nrep <= 8, ESGD_ERR_UNSUPPORTED, "sync_update_sum: at most 8 local replicas, got %d", nrep);
+  ESGD_REQUIRE(num_workers >= 1, ESGD_ERR_INPUT, "num_workers must be >= 1");
+  ESGD_REQUIRE(nrep == 1 || (ldw >= n && ldg >= n), ESGD_ERR_SHAPE,
+               "sync_update_sum: replica pitch (%lld, %lld) shorter than n=%lld", (long long)ldw,
+               (long long)ldg, (long long)n);
+  if (n == 0) return ESGD_OK;
+  ESGD_REQUIRE(W && G && C && S && S_next, ESGD_ERR_INPUT, "sync_update_sum: null buffer");
+  ESGD_REQUIRE(vec_ok({W, G, C, S, S_next}) && (nrep == 1 || ((ldw & 3) == 0 && (ldg & 3) == 0)),
+               ESGD_ERR_UNSUPPORTED, "sync_update_sum: buffers and pitches must be 16-B aligned");
+  const float p = (float)num_workers;
+  const int grid = stride_grid(n / 4 + 1, 256);
+  cudaStream_t st = ESGD_STREAM(stream);
+  if (nrep == 1) k_sync_update_sum4<1><<<grid, 256, 0, st>>>(W, ldw, G, ldg, nrep, C, S, S_next, n, eta, etarho, p);
+  else if (nrep == 2) k_sync_update_sum4<2><<<grid, 256, 0, st>>>(W, ldw, G, ldg, nrep, C, S, S_next, n, eta, etarho, p);
+  else if (nrep <= 4) k_sync_update_sum4<4><<<grid, 256, 0, st>>>(W, ldw, G, ldg, nrep, C, S, S_next, n, eta, etarho, p);
+  else k_sync_update_sum4<8><<<grid, 256, 0, st>>>(W, ldw, G, ldg, nrep, C, S, S_next, n, eta, etarho, p);
+  return check_launch("esgd_sync_update_sum_f32");
 }
 
 extern "C" int esgd_measgd_update_f32(float* w, float* v, const float* g, const float* c,

@@ -35,7 +35,7 @@ from ..errors import InputError
 from ..fabric.collectives import allreduce_sum_, local_workers, replica_sum_, world
 from ..fabric.engine import CATEGORIES
 from ..rng import stream_seed
-from ..updates import sync_update_
+from ..updates import sync_update_, sync_update_sum_
 from .common import Recorder
 from .config import TrainerConfig
 from .records import RunRecord
@@ -76,6 +76,12 @@ class SyncEngine:
         self.local_groups = max(1, self.nrep // gsize) if self.groups > 1 else 1
         self.partials = (torch.zeros((self.local_groups, ld), dtype=torch.float32, device=dev)
                          if self.local_groups > 1 else None)
+        # without groups the update kernel also forms the next round's local
+        # replica sum (esgd_sync_update_sum_f32), so S holds sum_r W_r at the
+        # start of every round and the round only allreduces it
+        self.fused_sum = self.groups == 1 and self.nrep <= 8
+        if self.fused_sum:
+            replica_sum_(self.S, self.W, self.n)
         self.plan = problem.bind(dev, self.nrep, cfg.batch_size, ld, use_tc=use_tc)
         self.plan.set_streams([stream_seed(cfg.seed, w) for w in range(self.first, self.first + self.nrep)])
         self.comm = torch.cuda.Stream(device=dev)
@@ -90,7 +96,9 @@ class SyncEngine:
 
     # ---- one round ------------------------------------------------------------
     def _sum(self, stream) -> None:
-        s = stream_ptr(stream)
+        if self.fused_sum:  # local sum already formed by the previous update
+            allreduce_sum_(self.S)
+            return
         if self.partials is not None:
             gsize = self.nrep // self.local_groups
             for g in range(self.local_groups):
@@ -104,7 +112,10 @@ class SyncEngine:
         self.plan.gradient(self.G, self.W, stream_ptr(stream))
 
     def _update(self, stream) -> None:
-        sync_update_(self.W, self.G, self.C, self.S, self.n, self.P, self.cfg.hyper, stream)
+        if self.fused_sum:
+            sync_update_sum_(self.W, self.G, self.C, self.S, self.S, self.n, self.P, self.cfg.hyper, stream)
+        else:
+            sync_update_(self.W, self.G, self.C, self.S, self.n, self.P, self.cfg.hyper, stream)
 
     def step_eager(self, ev: dict | None = None) -> None:
         cs = torch.cuda.current_stream()

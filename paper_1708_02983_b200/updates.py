@@ -144,6 +144,18 @@ def msgd_step(w, v, grad, eta: float, mu: float):
     return w2, v2
 
 
+def sync_update_sum_(W: torch.Tensor, G: torch.Tensor, C: torch.Tensor, S: torch.Tensor, S_next: torch.Tensor,
+                     n: int, num_workers: int, hyper: HyperParams, stream=None) -> None:
+    """sync_update_ plus the next round's local replica sum S_next =
+    tree_sum(W_r(t+1)) (fabric/collectives.py:18-32 order) in the same pass;
+    S_next may be S."""
+    if W.dim() != 2 or G.shape != W.shape:
+        raise ShapeError("sync_update_sum_: W and G must be (nrep, ld) with equal shapes")
+    _lib.call("esgd_sync_update_sum_f32", ptr(W), W.stride(0), ptr(G), G.stride(0), W.shape[0],
+              ptr(C), ptr(S), ptr(S_next), n, hyper.eta32, hyper.etarho32, int(num_workers),
+              stream_ptr(stream))
+
+
 def sync_update_(W: torch.Tensor, G: torch.Tensor, C: torch.Tensor, S: torch.Tensor, n: int,
                  num_workers: int, hyper: HyperParams, stream=None) -> None:
     """Fused Sync-EASGD round update for all local replicas (rows of W/G),

@@ -404,3 +404,26 @@ def test_stride2_maxpool_cnhw_batched(k, h, w):
         assert np.array_equal(host(am[z]), ea), z
         exp = O._maxpool_bwd(dys[z], ea, (n, c, h, w)) * (xs[z] > 0)
         assert np.array_equal(_from_cnhw(host(dx[z]), n, c, h, w), exp), z
+
+
+@pytest.mark.parametrize("nrep,n", [(1, 1031), (2, 4096), (3, 999), (5, 64), (8, 1027)])
+def test_sync_update_sum_equals_update_then_tree_sum(nrep, n):
+    """esgd_sync_update_sum_f32 == esgd_sync_update_f32 followed by the
+    replica tree sum of the updated replicas, bit for bit (S_next aliasing S)"""
+    rng = np.random.default_rng(nrep * 100 + n)
+    ld = (n + 63) // 64 * 64
+    W0 = rng.standard_normal((nrep, ld)).astype(np.float32)
+    G0 = rng.standard_normal((nrep, ld)).astype(np.float32)
+    C0 = rng.standard_normal(ld).astype(np.float32)
+    S0 = rng.standard_normal(ld).astype(np.float32)
+    hy = U.HyperParams(eta=0.05, rho=0.25)
+    W1, G1, C1, S1 = dev(W0), dev(G0), dev(C0), dev(S0)
+    U.sync_update_(W1, G1, C1, S1, n, 7, hy)
+    T1 = torch.zeros(ld, device="cuda")
+    collectives.replica_sum_(T1, W1, n)
+    W2, G2, C2, S2 = dev(W0), dev(G0), dev(C0), dev(S0)
+    U.sync_update_sum_(W2, G2, C2, S2, S2, n, 7, hy)
+    torch.cuda.synchronize()
+    assert torch.equal(W1[:, :n], W2[:, :n])
+    assert torch.equal(C1[:n], C2[:n])
+    assert torch.equal(T1[:n], S2[:n])

@@ -1,6 +1,7 @@
 """Small, deterministic launch sequences for ncu captures (profiles/).
 
     python tools/ncu_case.py update     # fused elastic update on 61.1M params (AlexNet size), 5 launches
+    python tools/ncu_case.py update_sum # the same + next round's replica sum (the engine's round update)
     python tools/ncu_case.py dgrad      # tcgen05 conv2 dgrad GEMM (M=93312 N=1600 K=192), 4 launches
     python tools/ncu_case.py fwd        # tcgen05 conv2 forward GEMM (M=93312 N=192 K=1600), 4 launches
     python tools/ncu_case.py wgrad      # tcgen05 conv2 wgrad GEMM (M=192 N=1600 K=93312), 4 launches
@@ -18,10 +19,10 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1708_02983_b200 import HyperParams, _lib  # noqa: E402
 from paper_1708_02983_b200.device import stream_ptr  # noqa: E402
-from paper_1708_02983_b200.updates import sync_update_  # noqa: E402
+from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_  # noqa: E402
 
 
-def update():
+def update(fused=False):
     n = 61_100_840
     ld = (n + 63) // 64 * 64
     W = torch.randn((1, ld), device="cuda")
@@ -30,7 +31,10 @@ def update():
     S = torch.randn(ld, device="cuda")
     hy = HyperParams(eta=0.01, rho=0.1)
     for _ in range(5):
-        sync_update_(W, G, Cc, S, n, 8, hy)
+        if fused:
+            sync_update_sum_(W, G, Cc, S, S, n, 8, hy)
+        else:
+            sync_update_(W, G, Cc, S, n, 8, hy)
     torch.cuda.synchronize()
 
 
@@ -90,6 +94,8 @@ if __name__ == "__main__":
     case = sys.argv[1]
     if case == "update":
         update()
+    elif case == "update_sum":
+        update(fused=True)
     elif case == "dgrad":
         gemm(93312, 1600, 192, 1, 0, 1)
     elif case == "fwd":
