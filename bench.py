@@ -291,7 +291,8 @@ def run_device(args):
         "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs)",
         "data": "synthetic (gen_synthetic blobs, HBM-resident)",
-        "config": dict(workload_config(args, b, world), params=eng.n, graph=eng.graph is not None),
+        "config": dict(workload_config(args, b, world), params=eng.n, graph=eng.graph is not None,
+                       collective=eng.collective),
         "roofline": roof,
         "roofline_update": roof_upd,
         "comm_fraction_exposed": round(comm_frac, 4),
@@ -305,7 +306,7 @@ def run_device(args):
     if world > 1:
         # captured graphs hold NCCL work; tearing the communicator down under
         # them can hang, so release them, sync, and leave without a teardown
-        eng.graph = None
+        eng.graph, eng.graphs = None, [None, None]
         torch.cuda.synchronize()
         dist.barrier()
         sys.stdout.flush()
@@ -460,6 +461,7 @@ class HostStager:
         k = self.cur
         self.pending.result()                                # batch k staged on the host
         self._graph(k).replay()                              # H2D + round + loss D2H (async)
+        self.eng.advance()
         self.pending = self.pool.submit(self._stage_host, k ^ 1)  # stage the next batch meanwhile
         torch.cuda.current_stream().synchronize()
         self.cur = k ^ 1
@@ -550,6 +552,7 @@ class DmaStager(HostStager):
         cs = torch.cuda.current_stream()
         cs.wait_event(self.ev[k])      # batch k on the device
         self._graph(k).replay()        # round + loss D2H (async)
+        self.eng.advance()
         self._load(k ^ 1)              # next batch by DMA, concurrent with round k
         cs.synchronize()
         self.cur = k ^ 1

@@ -72,6 +72,37 @@ int esgd_sync_update_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg,
                              float* C, const float* S, float* S_next, int64_t n, float eta,
                              float etarho, int32_t num_workers, esgd_stream_t stream);
 
+/* Multi-GPU round update fused with its collective over NVLink SHARP
+ * (NVLS) multicast (replaces ncclAllReduce(S) + esgd_sync_update_sum_f32):
+ * this rank's 1/world slice of the center is updated from the NVSwitch-
+ * reduced sum of every rank's S (multimem.ld_reduce on S_mc) and broadcast
+ * to all ranks (multimem.st to C_new_mc); all local replicas take the worker
+ * step against C_old and S_next = their binomial tree sum. S_mc / C_new_mc
+ * are multicast addresses of symmetric buffers (torch symmetric memory);
+ * C_old, S_next local. n4 = padded length (multiple of 4, zero padding).
+ * Call esgd_nvls_barrier first (orders the previous round's writes/reads). */
+int esgd_sync_update_nvls_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
+                              const float* C_old, const float* S_mc, float* C_new_mc, float* S_next,
+                              int64_t n4, int32_t world, int32_t rank, float eta, float etarho,
+                              int32_t num_workers, esgd_stream_t stream);
+
+/* The same round split for overlap (what the engine runs): the center
+ * slice (NVLS ld_reduce -> center step -> multicast broadcast) on a side
+ * stream concurrently with the forward/backward (ctas = grid size, 0 = one
+ * per SM), and the local worker step + next replica sum after it.          */
+int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, float* C_new_mc, int64_t n4,
+                              int32_t world, int32_t rank, float etarho, int32_t num_workers, int32_t ctas,
+                              esgd_stream_t stream);
+int esgd_worker_step_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
+                             const float* C, float* S_next, int64_t n4, float eta, float etarho,
+                             esgd_stream_t stream);
+
+/* Cross-GPU barrier on the device: peer_flags = device array of world
+ * pointers to each rank's symmetric int32 flag array (>= world entries,
+ * zero-initialised); epoch = this rank's device counter (graph-replayable). */
+int esgd_nvls_barrier(int32_t* const* peer_flags, int32_t world, int32_t rank, int32_t* epoch,
+                      esgd_stream_t stream);
+
 /* measgd_worker_step, updates.py:134-140 (in place):
  *   v = mu*v - eta*g;  w = (w + v) - etarho*(w - c).  24 B/param.          */
 int esgd_measgd_update_f32(float* w, float* v, const float* g, const float* c, int64_t n,

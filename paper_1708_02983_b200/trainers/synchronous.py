@@ -33,6 +33,7 @@ import torch.distributed as dist
 from ..device import require_cuda, round_up, stream_ptr
 from ..errors import InputError
 from ..fabric.collectives import allreduce_sum_, local_workers, replica_sum_, world
+from ..fabric.nvls import NvlsRound, nvls_fused_single_kernel, nvls_wanted
 from ..fabric.engine import CATEGORIES
 from ..rng import stream_seed
 from ..updates import sync_update_, sync_update_sum_
@@ -82,6 +83,10 @@ class SyncEngine:
         self.fused_sum = self.groups == 1 and self.nrep <= 8
         if self.fused_sum:
             replica_sum_(self.S, self.W, self.n)
+        # multi-GPU: the round's collective + update as ONE kernel over NVLink
+        # SHARP multicast (fabric/nvls.py, csrc/nvls.cu) when the fabric has it;
+        # otherwise one NCCL allreduce of S per round
+        self.nvls, self.parity = None, 0
         self.plan = problem.bind(dev, self.nrep, cfg.batch_size, ld, use_tc=use_tc)
         self.plan.set_streams([stream_seed(cfg.seed, w) for w in range(self.first, self.first + self.nrep)])
         self.comm = torch.cuda.Stream(device=dev)
@@ -93,9 +98,28 @@ class SyncEngine:
         if self.world > 1:  # bring NCCL up outside any capture
             allreduce_sum_(torch.zeros(1, device=dev))
             torch.cuda.synchronize()
+            if self.fused_sum and nvls_wanted():
+                try:
+                    self.nvls = NvlsRound(ld, dev)
+                except Exception:  # no multicast object support: NCCL path
+                    self.nvls = None
+                    torch.cuda.synchronize()
+            if self.nvls is not None:
+                self.nvls.C[0].copy_(self.C)
+                self.nvls.S[0].copy_(self.S)
+                self.C, self.S = self.nvls.C[0], self.nvls.S[0]
+                torch.cuda.synchronize()
+        self.graphs = [None, None]
+        self.nvls_single = nvls_fused_single_kernel()
+        self.collective = ("nvls-fused" if self.nvls is not None else
+                           ("nccl-allreduce" if self.world > 1 else "none"))
 
     # ---- one round ------------------------------------------------------------
     def _sum(self, stream) -> None:
+        if self.nvls is not None:
+            if not self.nvls_single:  # center slice over NVLS, overlapped with the backward
+                self.nvls.center(self.parity, self.P, self.cfg.hyper, stream)
+            return
         if self.fused_sum:  # local sum already formed by the previous update
             allreduce_sum_(self.S)
             return
@@ -112,7 +136,12 @@ class SyncEngine:
         self.plan.gradient(self.G, self.W, stream_ptr(stream))
 
     def _update(self, stream) -> None:
-        if self.fused_sum:
+        if self.nvls is not None:
+            if self.nvls_single:
+                self.nvls.update(self.W, self.G, self.parity, self.P, self.cfg.hyper, stream)
+            else:
+                self.nvls.workers(self.W, self.G, self.parity, self.cfg.hyper, stream)
+        elif self.fused_sum:
             sync_update_sum_(self.W, self.G, self.C, self.S, self.S, self.n, self.P, self.cfg.hyper, stream)
         else:
             sync_update_(self.W, self.G, self.C, self.S, self.n, self.P, self.cfg.hyper, stream)
@@ -152,12 +181,25 @@ class SyncEngine:
         torch.cuda.current_stream().wait_stream(s)
         if rng_before is not None:  # capture does not execute, but keep state untouched
             self.plan.rng.state.copy_(rng_before)
+        if self.nvls is not None:
+            self.graphs[self.parity] = g
+        else:
+            self.graphs = [g, g]
         self.graph = g
 
+    def advance(self) -> None:
+        """After a round: the NVLS path double-buffers S/C by round parity."""
+        if self.nvls is not None:
+            self.parity ^= 1
+            self.C, self.S = self.nvls.C[self.parity], self.nvls.S[self.parity]
+
     def step(self) -> None:
-        """Enqueue one round (graph replay once captured)."""
-        if self.graph is not None:
-            self.graph.replay()
+        """Enqueue one round (graph replay once captured; the NVLS path keeps
+        one graph per round parity)."""
+        k = self.parity
+        if self.graphs[k] is not None:
+            self.graphs[k].replay()
+            self.advance()
             return
         if self.use_graph and self.profiled >= self.profile_rounds:
             try:
@@ -165,13 +207,15 @@ class SyncEngine:
             except Exception:  # capture unsupported here (e.g. NCCL): stay eager
                 self.use_graph = False
                 torch.cuda.synchronize()
-            if self.graph is not None:
-                self.graph.replay()
+            if self.graphs[k] is not None:
+                self.graphs[k].replay()
+                self.advance()
                 return
         if self.profiled < self.profile_rounds:
             self._profiled_step()
         else:
             self.step_eager()
+        self.advance()
 
     def _profiled_step(self) -> None:
         names = ("t0", "c0", "c1", "g1", "j", "u1")
@@ -237,6 +281,6 @@ def run_synchronous(cfg: TrainerConfig, problem, cm=None, **engine_kw) -> RunRec
             t0.record()
     total = _max_over_ranks(elapsed, eng.device)
     info = {"engine": "cuda", "world": eng.world, "replicas_per_rank": eng.nrep,
-            "graph": eng.graph is not None, "overlap": eng.overlap}
+            "graph": eng.graph is not None, "overlap": eng.overlap, "collective": eng.collective}
     return rec.build(cfg.method, total, eng.center_host(), breakdown=eng.breakdown(total),
                      worker_weights=eng.workers_host(), engine_info=info)

@@ -2,6 +2,7 @@
 round's CUDA graph) — runs only where >= 2 GPUs are visible; equality with
 the single-process run is bitwise at N = 2 (tools/dist_check.py)."""
 
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -14,8 +15,13 @@ ROOT = Path(__file__).resolve().parent.parent
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_two_rank_sync_easgd_equals_single_process():
+@pytest.mark.parametrize("nvls", ["1", "0"])
+def test_two_rank_sync_easgd_equals_single_process(nvls):
+    """NVLS-fused round update (multimem ld_reduce / st over NVSwitch) and the
+    NCCL-allreduce path both equal the single-process run bit for bit."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29531", str(ROOT / "tools" / "dist_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, ESGD_NVLS=nvls)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert "DIST_CHECK PASS" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    print(r.stdout[-400:])
