@@ -64,9 +64,12 @@ struct Cfg {
   static constexpr int kOffBLo = kOffB + kTileBytesB;
   static constexpr int kStageBytes = kTileBytesA + kTileBytesB * (SPLIT ? 2 : 1);
   static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
-  static constexpr int kACol0 = 2 * BN;  // TMEM columns of the A regions (64 per stage: hi 32 | lo 32)
+  static constexpr int kACol0 = 2 * BN;  // TMEM columns of the A regions (64 per slot: hi 32 | lo 32)
+  // TMEM A slots (a ring of its own): as many as the 512 columns leave next to
+  // the two BN-wide accumulators — 4 at BN <= 128, 2 at BN = 192
+  static constexpr int kASlots = SPLIT ? ((512 - 2 * BN) / 64 < kStages ? (512 - 2 * BN) / 64 : kStages) : 1;
   static constexpr int kTmemCols = SPLIT ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
-  static_assert(!SPLIT || kACol0 + 64 * kStages <= 512, "TMEM budget");
+  static_assert(!SPLIT || (kASlots >= 2 && kACol0 + 64 * kASlots <= 512), "TMEM budget");
   static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
   static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -285,7 +288,8 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 
 template <int BYTES>
 __device__ __forceinline__ void split_tile(uint32_t raw, uint32_t lo, int tid) {
-  constexpr int kVec = BYTES / 16, kPer = kVec / 128, kBatch = kPer < 8 ? kPer : 8;
+  constexpr int kVec = BYTES / 16, kPer = kVec / 128;
+  constexpr int kBatch = kPer <= 8 ? kPer : (kPer % 8 == 0 ? 8 : (kPer % 6 == 0 ? 6 : 4));
   static_assert(kVec % 128 == 0 && kPer % kBatch == 0, "tile must split evenly over 128 threads");
 #pragma unroll
   for (int b0 = 0; b0 < kPer; b0 += kBatch) {
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t acc0 = (kb > kc || kk > 0) ? 1u : 0u;
               if (SPLIT) {
                 const uint64_t bl = op_desc<BMN>(st + C::kOffBLo, kk);
-                const uint32_t ahi = tmem + C::kACol0 + s * 64 + kk * 8, alo = ahi + 32;
+                const uint32_t ahi = tmem + C::kACol0 + (g % C::kASlots) * 64 + kk * 8, alo = ahi + 32;
                 mma_tf32_ts(acc, alo, bh, idesc_ts, acc0);  // small terms first
                 mma_tf32_ts(acc, ahi, bl, idesc_ts, 1u);
                 mma_tf32_ts(acc, ahi, bh, idesc_ts, 1u);
@@ -537,7 +541,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               lo[k] = __float_as_uint(__fsub_rn(x, h));
             }
           }
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + C::kACol0 + s * 64;
+          // TMEM A slot g % kASlots: free once the MMAs of k-block g - kASlots
+          // retired (their commit completes that k-block's smem-stage phase)
+          if (C::kASlots < C::kStages && g >= (uint32_t)C::kASlots) {
+            const uint32_t gp = g - C::kASlots;
+            mbar_wait(empty0 + 8 * (gp % C::kStages), (gp / C::kStages) & 1);
+            tc_fence_after();
+          }
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + C::kACol0 + (g % C::kASlots) * 64;
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
           split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
@@ -570,13 +581,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = c & 1;
         mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
         tc_fence_after();
+        if (HB <= 64) {
 #pragma unroll
-        for (int c0 = 0; c0 < HB; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + h * HB + c0, v);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < HB; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + h * HB + c0, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], __uint_as_float(v[j]));
+            for (int j = 0; j < 32; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], __uint_as_float(v[j]));
+          }
+        } else {  // BN = 192: 96 accumulators per thread leave room for 16-column loads only
+#pragma unroll
+          for (int c0 = 0; c0 < HB; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + h * HB + c0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -704,6 +725,23 @@ int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64
   return ESGD_OK;
 }
 
+// N tile width. 192-wide tiles (3 smem stages, 2 TMEM A slots) only where
+// they strictly cut the padded MMA columns (N = 192: conv2 forward and, after
+// the orientation swap, its weight gradient; measured 0.34 -> 0.25 ms and
+// 0.40 -> 0.30 ms). On ties or near-ties the deeper 128-wide pipeline won
+// (N = 1600 / 4096 / 9216 measured 5-18% slower at 192).
+inline int64_t padded(int64_t n, int bn) { return ((n + bn - 1) / bn) * bn; }
+inline int pick_bn(int64_t n, bool split) {
+  static const int force = getenv("ESGD_TC_BN") ? atoi(getenv("ESGD_TC_BN")) : 0;  // tuning runs
+  if (force == 64 || force == 128 || (force == 192 && split)) return force;
+  if (n <= 64) return 64;
+  return (split && padded(n, 192) < padded(n, 128)) ? 192 : 128;
+}
+// padded MMA area of an orientation (M tiled by 128, N by the chosen width)
+inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
+  return padded(m, BM) * padded(n, pick_bn(n, split));
+}
+
 template <int BN, bool SPLIT, bool AMN, bool BMN>
 int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   using C = Cfg<BN, SPLIT>;
@@ -804,7 +842,22 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
                ESGD_ERR_UNSUPPORTED, "tc_gemm: too many tiles");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool split = d->precision == 3;
-  if (d->n <= 64)
-    return split ? tc::launch_major<64, true>(d, st) : tc::launch_major<64, false>(d, st);
-  return split ? tc::launch_major<128, true>(d, st) : tc::launch_major<128, false>(d, st);
+  // Orientation: C^T = B . A^T is the same GEMM with the operands' roles
+  // swapped; take it when it needs less padded tensor-core work (M is tiled
+  // by 128: a 64- or 192-row M wastes half / a quarter of every MMA). Only
+  // without a per-column bias (the epilogue applies bias along N).
+  esgd_tc_gemm_desc sw = *d;
+  const esgd_tc_gemm_desc* use = d;
+  if (!d->bias && tc::padded_cost(d->n, d->m, split) < tc::padded_cost(d->m, d->n, split)) {
+    sw.m = d->n; sw.n = d->m;
+    sw.a = d->b; sw.lda = d->ldb; sw.a_sb = d->b_sb; sw.a_major = d->b_major;
+    sw.b = d->a; sw.ldb = d->lda; sw.b_sb = d->a_sb; sw.b_major = d->a_major;
+    sw.c_sm = d->c_sn; sw.c_sn = d->c_sm;
+    sw.mask_sm = d->mask_sn; sw.mask_sn = d->mask_sm;
+    use = &sw;
+  }
+  const int bn = tc::pick_bn(use->n, split);
+  if (bn == 64) return split ? tc::launch_major<64, true>(use, st) : tc::launch_major<64, false>(use, st);
+  if (bn == 192) return tc::launch_major<192, true>(use, st);
+  return split ? tc::launch_major<128, true>(use, st) : tc::launch_major<128, false>(use, st);
 }

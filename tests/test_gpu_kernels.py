@@ -427,3 +427,34 @@ def test_sync_update_sum_equals_update_then_tree_sum(nrep, n):
     assert torch.equal(W1[:, :n], W2[:, :n])
     assert torch.equal(C1[:n], C2[:n])
     assert torch.equal(T1[:n], S2[:n])
+
+
+@pytest.mark.parametrize("m,n,k,a_major,b_major,bias", [
+    (500, 192, 300, 1, 0, True),     # BN = 192 tile, bias + relu epilogue (conv2 forward shape class)
+    (300, 384, 200, 0, 0, False),    # BN = 192, two n tiles
+    (192, 1600, 4096, 0, 0, False),  # M = 192 weight gradient: swapped orientation, BN = 192, split-K
+    (64, 363, 20000, 0, 0, False),   # M = 64 weight gradient: swapped orientation, split-K
+    (1000, 1600, 192, 1, 0, False),  # dgrad shape class, BN = 192 with a padded last tile
+])
+def test_tcgen05_gemm_wide_tiles_and_orientation(m, n, k, a_major, b_major, bias):
+    """the 192-wide N tiles (TMEM A ring of 2) and the padded-work orientation
+    choice (C^T = B.A^T) against an fp64 reference"""
+    rng = np.random.default_rng(m + n + k)
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((n, k)).astype(np.float32)
+    As = np.ascontiguousarray(A.T) if a_major else A
+    Bs = np.ascontiguousarray(B.T) if b_major else B
+    lda, ldb = (m if a_major else k), (n if b_major else k)
+    bvec = rng.standard_normal(n).astype(np.float32)
+    Ad, Bd, bd = dev(As), dev(Bs), dev(bvec)
+    Cd = torch.zeros((m, n), device="cuda")
+    ws = torch.zeros(1 << 24, device="cuda")
+    d = _lib.TcGemmDesc(m, n, k, 1, Ad.data_ptr(), lda, 0, Bd.data_ptr(), ldb, 0, Cd.data_ptr(), n, 1, 0,
+                        bd.data_ptr() if bias else None, 0, None, 0, 0, 0, 1 if bias else 0, 0, 3,
+                        a_major, b_major, ws.data_ptr(), ws.numel())
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    torch.cuda.synchronize()
+    ref = _gemm_ref(A, B.T)
+    if bias:
+        ref = np.maximum(ref + bvec.astype(np.float64), 0.0)
+    assert rel_err(host(Cd), ref) < 3e-6, rel_err(host(Cd), ref)
