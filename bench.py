@@ -203,7 +203,7 @@ def time_dominant_gemm(eng, reps: int = 10):
         t = a.elapsed_time(b) / reps / 1e3
         if best is None or t > best[2]:
             best = (f"m={d.m} n={d.n} k={d.k} batch={d.batch} a_major={d.a_major} b_major={d.b_major}",
-                    flops, t, d.precision)
+                    flops, t, d.precision, f"tc_gemm:{d.m}x{d.n}x{d.k}")
     return best
 
 
@@ -267,12 +267,12 @@ def run_device(args):
     # against the measured bf16 peak / 2 (nominal dense tf32 = bf16 / 2)
     dom = time_dominant_gemm(eng)
     if dom is not None:
-        desc, fl, t, prec = dom
+        desc, fl, t, prec, tkey = dom
         tf32_peak = pk.get("bf16_tflops", 1590.0) / 2
         ach = prec * fl / t / 1e12
         roof = {"kernel": f"esgd_tc_gemm_f32 (k_tc_gemm, {desc})", "bound": "tensor",
                 "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                "frac": round(ach / tf32_peak, 4), "traffic": traffic("tc_gemm_dominant", args.model),
+                "frac": round(ach / tf32_peak, 4), "traffic": traffic(tkey, args.model),
                 "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
                 "algorithmic_flops_per_launch": fl,
                 "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)"}
