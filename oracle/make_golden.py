@@ -159,11 +159,44 @@ def async_fixture():
     return d
 
 
+def formats_fixture():
+    """Bytes written by the reference's IDX writer and EFW1 checkpointer
+    (datasets.py:111-126, network.py:203-211), and what its loaders read
+    back, for the format round-trip tests."""
+    import os
+    import tempfile
+
+    from elasticsgd.datasets import load_idx, write_idx
+    from elasticsgd.network import PackedWeights, build_model, load_weights, save_weights  # noqa: F401
+
+    d = {}
+    ds = normalize(gen_synthetic(3, 12, 4, seed=9, separation=5.0))
+    samples01 = (ds.samples - ds.samples.min()) / (ds.samples.max() - ds.samples.min())
+    with tempfile.TemporaryDirectory() as tmp:
+        ip, lp = os.path.join(tmp, "img.idx"), os.path.join(tmp, "lab.idx")
+        write_idx(ip, lp, samples01, ds.labels, rows=3, cols=4)
+        d["idx_images"] = np.frombuffer(open(ip, "rb").read(), dtype=np.uint8)
+        d["idx_labels"] = np.frombuffer(open(lp, "rb").read(), dtype=np.uint8)
+        back = load_idx(ip, lp)
+        d["idx_samples"], d["idx_labels_loaded"] = back.samples, back.labels
+        d["idx_input"] = samples01
+        d["idx_input_labels"] = ds.labels
+        spec = ModelSpec((5, 4, 3), seed=2)
+        model = build_model(spec)
+        cp = os.path.join(tmp, "w.efw1")
+        save_weights(cp, spec, model)
+        d["efw1_bytes"] = np.frombuffer(open(cp, "rb").read(), dtype=np.uint8)
+        dims, buf = load_weights(cp)
+        d["efw1_dims"], d["efw1_buf"] = np.array(dims), buf
+    return d
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     only = sys.argv[1:]
     for name, fn in (("rng", rng_fixture), ("data", data_fixture), ("updates", update_fixture),
-                     ("net", net_fixture), ("trainers", trainer_fixture), ("async", async_fixture)):
+                     ("net", net_fixture), ("trainers", trainer_fixture), ("async", async_fixture),
+                     ("formats", formats_fixture)):
         if only and name not in only:
             continue
         path = OUT / f"{name}.npz"

@@ -104,3 +104,7 @@ def standardize_pair(train: Dataset, test: Dataset) -> tuple[Dataset, Dataset]:
         return Dataset(out, d.labels.copy(), d.num_classes)
 
     return apply(train), apply(test)
+
+
+# IDX pairs (reference datasets.py:82-126), implemented in formats.py
+from .formats import load_idx, write_idx  # noqa: E402,F401

@@ -292,3 +292,7 @@ def alexnet(seed: int = 0, dtype=np.float32, num_classes: int = 1000) -> ConvNet
 
 
 MODELS = {"lenet": lenet, "cifar-quick": cifar_quick, "alexnet": alexnet}
+
+
+# EFW1 checkpoints (reference network.py:203-233), implemented in formats.py
+from .formats import load_weights, save_weights  # noqa: E402,F401

@@ -187,6 +187,13 @@ class SyncEngine:
             self.graphs = [g, g]
         self.graph = g
 
+    def after_external_write(self) -> None:
+        """W / C were overwritten outside the round (resume): re-form the local
+        replica sum the fused update path keeps in S."""
+        if self.fused_sum:
+            replica_sum_(self.S, self.W, self.n)
+        torch.cuda.synchronize()
+
     def advance(self) -> None:
         """After a round: the NVLS path double-buffers S/C by round parity."""
         if self.nvls is not None:

@@ -112,3 +112,38 @@ def test_sync_cnn_multi_replica_vs_oracle(model, tc, monkeypatch):
     assert rel_err(rec.final_weights, C) < 1e-4
     for w_dev, w_ref in zip(rec.final_worker_weights, W):
         assert rel_err(w_dev, w_ref) < 1e-4
+
+
+@pytest.mark.parametrize("model", ["mlp", "lenet"])
+def test_resume_from_state_is_bitwise(model, golden, tmp_path):
+    """ESR1 save / load (formats.py): 3 rounds, checkpoint,
+    a fresh engine restored from it, 3 more rounds == 6 rounds straight."""
+    import torch
+
+    from paper_1708_02983_b200 import formats, network
+    from paper_1708_02983_b200.trainers.synchronous import SyncEngine
+
+    if model == "mlp":
+        prob = _mlp_problem(golden)
+    else:
+        rng = np.random.default_rng(3)
+        prob = NetworkProblem(network.lenet(seed=0), Dataset(rng.standard_normal((300, 784)),
+                                                             rng.integers(0, 10, 300), 10))
+    cfg = make_config("sync-easgd3", workers=3, iterations=6, batch_size=8, hyper=HY, seed=4)
+
+    def rounds(eng, k):
+        for _ in range(k):
+            eng.step()
+        torch.cuda.synchronize()
+
+    a = SyncEngine(cfg, prob)
+    rounds(a, 6)
+    b = SyncEngine(cfg, prob)
+    rounds(b, 3)
+    formats.save_state(tmp_path / "s.esr1", b, 3)
+    c = SyncEngine(cfg, prob)
+    assert formats.load_state(tmp_path / "s.esr1", c) == 3
+    rounds(c, 3)
+    assert np.array_equal(a.center_host(), c.center_host())
+    for wa, wc in zip(a.workers_host(), c.workers_host()):
+        assert np.array_equal(wa, wc)

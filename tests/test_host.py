@@ -114,3 +114,22 @@ def test_model_specs_validate():
         network.ConvNetSpec((1, 8, 8), (network.Conv(4, 3),))
     with pytest.raises(Exception):
         network.ConvNetSpec((1, 4, 4), (network.Conv(4, 7), network.Dense(2)))
+
+
+def test_costmodel_recalibration_helpers():
+    """alpha-beta fit, the B200 preset, and the sync-round
+    predictor (overlap: no exposed comm while compute covers it)."""
+    from paper_1708_02983_b200.fabric import costmodel as cmod
+
+    a, b = cmod.fit_alpha_beta([1e3, 1e6, 1e8], [2e-6 + 1e3 * 3e-12, 2e-6 + 1e6 * 3e-12, 2e-6 + 1e8 * 3e-12])
+    assert abs(a - 2e-6) < 1e-9 and abs(b - 3e-12) < 1e-15
+    cm = cmod.CostModel.preset("b200-nvlink")
+    assert cm.alpha > 0 and cm.beta > 0
+    one = cmod.predict_sync_round(cm, 4e-3, 61_100_840, 1)
+    assert one["comm_seconds"] == 0 and one["weak_scaling_efficiency"] == 1.0
+    eight = cmod.predict_sync_round(cm, 4e-3, 61_100_840, 8, interference=0.0)
+    assert eight["exposed_comm_seconds"] == 0.0 and eight["weak_scaling_efficiency"] == 1.0
+    tiny = cmod.predict_sync_round(cm, 1e-6, 61_100_840, 8)
+    assert tiny["exposed_comm_seconds"] > 0 and tiny["weak_scaling_efficiency"] < 0.1
+    pc = cmod.packed_vs_perlayer_cost([100, 200, 300], cm)
+    assert abs(pc.per_layer - pc.packed - 2 * cm.alpha) < 1e-15
