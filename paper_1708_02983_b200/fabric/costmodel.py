@@ -66,8 +66,8 @@ class CostModel:
 
 # measured on this pool's HGX B200 (NVLink 5 / NVSwitch): ncclAllReduce of the
 # packed fp32 buffer, fitted by calibrate_allreduce (profiles/r01_costmodel.md)
-B200_NVLINK_ALPHA = 28e-6
-B200_NVLINK_BETA = 1.0 / 330e9
+B200_NVLINK_ALPHA = 29.1e-6
+B200_NVLINK_BETA = 1.0 / 407.7e9
 
 _PRESETS = {
     "fdr": (0.7e-6, 0.2e-9),
