@@ -725,21 +725,24 @@ int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64
   return ESGD_OK;
 }
 
-// N tile width. 192-wide tiles (3 smem stages, 2 TMEM A slots) only where
-// they strictly cut the padded MMA columns (N = 192: conv2 forward and, after
-// the orientation swap, its weight gradient; measured 0.34 -> 0.25 ms and
-// 0.40 -> 0.30 ms). On ties or near-ties the deeper 128-wide pipeline won
-// (N = 1600 / 4096 / 9216 measured 5-18% slower at 192).
+// N tile width. 192-wide tiles (3 smem stages, 2 TMEM A slots) read the
+// TS-mode A operand from TMEM once per 192 instead of 128 output columns, so
+// they win wherever they do not add padding and there are enough M tiles to
+// fill the SMs (measured: conv2 fwd N=192 0.34 -> 0.25 ms, conv3 fwd N=384
+// 0.154 -> 0.143, conv4 dgrad N=3456 0.201 -> 0.189); with more padding
+// (N = 1600) or a single M tile (the FC layers, M = batch) 128 stays faster.
 inline int64_t padded(int64_t n, int bn) { return ((n + bn - 1) / bn) * bn; }
-inline int pick_bn(int64_t n, bool split) {
+inline int pick_bn(int64_t m, int64_t n, bool split) {
   static const int force = getenv("ESGD_TC_BN") ? atoi(getenv("ESGD_TC_BN")) : 0;  // tuning runs
   if (force == 64 || force == 128 || (force == 192 && split)) return force;
   if (n <= 64) return 64;
-  return (split && padded(n, 192) < padded(n, 128)) ? 192 : 128;
+  if (!split) return 128;
+  if (padded(n, 192) < padded(n, 128)) return 192;
+  return (padded(n, 192) == padded(n, 128) && m >= 16 * BM) ? 192 : 128;
 }
 // padded MMA area of an orientation (M tiled by 128, N by the chosen width)
 inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
-  return padded(m, BM) * padded(n, pick_bn(n, split));
+  return padded(m, BM) * padded(n, pick_bn(m, n, split));
 }
 
 template <int BN, bool SPLIT, bool AMN, bool BMN>
@@ -856,7 +859,7 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
     sw.mask_sm = d->mask_sn; sw.mask_sn = d->mask_sm;
     use = &sw;
   }
-  const int bn = tc::pick_bn(use->n, split);
+  const int bn = tc::pick_bn(use->m, use->n, split);
   if (bn == 64) return split ? tc::launch_major<64, true>(use, st) : tc::launch_major<64, false>(use, st);
   if (bn == 192) return tc::launch_major<192, true>(use, st);
   return split ? tc::launch_major<128, true>(use, st) : tc::launch_major<128, false>(use, st);
