@@ -28,14 +28,45 @@ class WorkerSlot:
             self.plan = problem.bind(device, 1, batch_size, self.ld, use_tc=use_tc)
             self.plan.set_streams([stream_seed(seed, wid)])
         self.done = 0
+        self.graph = None
+        self.calls = 0
 
     @property
     def s(self) -> int:
         return stream_ptr(self.stream)
 
     def gradient(self) -> None:
+        """Enqueue this worker's sample + forward/backward on its stream. After
+        one eager call the sequence is captured as a CUDA graph (the sampling
+        kernel advances the worker's RNG counter on the device, so replays draw
+        the next batches): a replay is one host call instead of ~30 launches,
+        which is what bounds the asynchronous schedules' throughput."""
         with torch.cuda.device(self.device):
-            self.plan.gradient(self.G, self.W, self.s)
+            if self.graph is None and self.calls >= 1:
+                self._capture()
+            if self.graph is not None:
+                with torch.cuda.stream(self.stream):
+                    self.graph.replay()
+            else:
+                self.plan.gradient(self.G, self.W, self.s)
+            self.calls += 1
+
+    def _capture(self) -> None:
+        rng = getattr(self.plan, "rng", None)
+        before = rng.state.clone() if rng is not None else None
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(self.stream)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                self.plan.gradient(self.G, self.W, stream_ptr(side))
+        except Exception:  # capture unsupported: stay eager
+            torch.cuda.synchronize(self.device)
+            return
+        self.stream.wait_stream(side)
+        if before is not None:  # capture does not execute; keep the RNG where it was
+            rng.state.copy_(before)
+        self.graph = g
 
     def w(self) -> torch.Tensor:
         return self.W[0, :self.n]

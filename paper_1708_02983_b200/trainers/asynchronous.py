@@ -141,8 +141,8 @@ def run_asynchronous(cfg: TrainerConfig, problem, cm=None, devices=None) -> RunR
             serve(w)
             services += 1
             if rec.due(services):
+                master.synchronize()  # the queued exchanges up to here are run time, not eval time
                 p0 = time.perf_counter()
-                master.synchronize()
                 rec.record(services, p0 - t_start - paused, C[:n])
                 paused += time.perf_counter() - p0
         waiting = [w for w in range(P) if slots[w].done < quotas[w]]
