@@ -176,6 +176,31 @@ __global__ void __launch_bounds__(256) k_im2col_sq(float* __restrict__ col, int6
   }
 }
 
+// im2col for big square kernels with few channels (AlexNet conv1: 3 x 11 x 11,
+// stride 4): one work item per (output pixel, channel, kernel row) — KS taps —
+// so the 363-deep K of three channels spreads over 33x more threads than one
+// pixel's full column (which left the launch at ~1.3 waves with long loops).
+template <int KS>
+__global__ void __launch_bounds__(256) k_im2col_rows(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
+                                                     const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
+                                                     int stride, int pad, int oh, int ow) {
+  const int z = blockIdx.z;
+  const int ohw = oh * ow, np = xd.n * ohw;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= np) return;
+  const int c = blockIdx.y / KS, ky = blockIdx.y - c * KS;
+  const int img = pix / ohw, p = pix - img * ohw, oy = p / ow, ox = p - oy * ow;
+  const int iy = oy * stride - pad + ky, ix0 = ox * stride - pad;
+  float* cp = col + z * col_sb + (int64_t)(c * KS * KS + ky * KS) * col_sk + pix;
+  const bool rok = iy >= 0 && iy < xd.h;
+  const float* rp = x + z * x_sb + img * xd.sn + (int64_t)c * xd.sc + (int64_t)iy * xd.sh + ix0;
+  float v[KS];
+#pragma unroll
+  for (int kx = 0; kx < KS; ++kx) v[kx] = (rok && ix0 + kx >= 0 && ix0 + kx < xd.w) ? __ldg(rp + kx) : 0.f;
+#pragma unroll
+  for (int kx = 0; kx < KS; ++kx) cp[(int64_t)kx * col_sk] = v[kx];
+}
+
 // col2im from colT: thread <-> input pixel (img, y, x), channels of a group;
 // (ky, kx) accumulation order fixed per element.
 template <bool STRIDE1>
@@ -216,7 +241,7 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
 // KS*KS loads of a channel are issued together (predicated), then summed in
 // the same (ky, kx) order as k_col2im_t, so results are identical
 template <int KS>
-__global__ void __launch_bounds__(256) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+__global__ void __launch_bounds__(256, KS >= 5 ? 4 : 1) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                    const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                    int pad, int oh, int ow, const float* __restrict__ mask,
                                                    int64_t mask_sb, int grp) {
@@ -226,27 +251,34 @@ __global__ void __launch_bounds__(256) k_col2im_sq(float* __restrict__ dx, esgd_
   if (q >= npin) return;
   const int img = q / hw, p = q - img * hw, yh = p / xd.w, xw = p - yh * xd.w;
   const float* dz = dcol + z * col_sb + (int64_t)img * oh * ow;
-  // tap validity and pixel offsets are per-thread constants
-  int off[KS * KS];
-  bool ok[KS * KS];
+  // tap validity as row/column bit masks; the tap addresses walk from the
+  // (0,0) tap's pixel (few registers: 4 CTAs of 256 threads per SM)
+  uint32_t rowok = 0, colok = 0;
 #pragma unroll
-  for (int ky = 0; ky < KS; ++ky)
-#pragma unroll
-    for (int kx = 0; kx < KS; ++kx) {
-      const int oy = yh + pad - ky, ox = xw + pad - kx;
-      ok[ky * KS + kx] = oy >= 0 && oy < oh && ox >= 0 && ox < ow;
-      off[ky * KS + kx] = oy * ow + ox;
-    }
+  for (int t = 0; t < KS; ++t) {
+    rowok |= (uint32_t)(yh + pad - t >= 0 && yh + pad - t < oh) << t;
+    colok |= (uint32_t)(xw + pad - t >= 0 && xw + pad - t < ow) << t;
+  }
+  const int base = (yh + pad) * ow + (xw + pad);
   const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
+#pragma unroll(KS <= 3 ? 2 : 1)
   for (int ci = c0; ci < c1; ++ci) {
-    const float* dc = dz + (int64_t)(ci * KS * KS) * col_sk;
+    const float* dc = dz + (int64_t)(ci * KS * KS) * col_sk + base;
     float v[KS * KS];
 #pragma unroll
-    for (int t = 0; t < KS * KS; ++t) v[t] = ok[t] ? __ldg(dc + (int64_t)t * col_sk + off[t]) : 0.f;
+    for (int ky = 0; ky < KS; ++ky) {
+      const float* rp = dc + (int64_t)(ky * KS) * col_sk - ky * ow;
+      const bool rk = (rowok >> ky) & 1u;
+#pragma unroll
+      for (int kx = 0; kx < KS; ++kx)
+        v[ky * KS + kx] = (rk && ((colok >> kx) & 1u)) ? __ldg(rp + (int64_t)kx * col_sk - kx) : 0.f;
+    }
     float acc = 0.f;
 #pragma unroll
-    for (int t = 0; t < KS * KS; ++t)
-      if (ok[t]) acc += v[t];
+    for (int ky = 0; ky < KS; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < KS; ++kx)
+        if (((rowok >> ky) & 1u) && ((colok >> kx) & 1u)) acc += v[ky * KS + kx];
     const int64_t o = img * xd.sn + ci * xd.sc + yh * xd.sh + xw * xd.sw;
     if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
     dx[z * x_sb + o] = acc;
@@ -627,7 +659,10 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
       k_im2col_sq<3><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
     else if (kh == 5)
       k_im2col_sq<5><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
-    else
+    else if (xd.c * kh <= 65535) {
+      dim3 g3((unsigned)((np + 255) / 256), (unsigned)(xd.c * kh), batch);
+      k_im2col_rows<11><<<g3, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow);
+    } else
       k_im2col_sq<11><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
     return check_launch("esgd_im2col_f32");
   }
