@@ -1,0 +1,66 @@
+"""C-ABI argument validation (include/esgd.h): every entry point checks its
+arguments before touching the device, returns ESGD_ERR_SHAPE / ESGD_ERR_INPUT
+with a message in esgd_last_error(), and zero-length work is a no-op — the
+reference's ShapeError / InputError contract (updates.py:32-38, 65-68). No
+kernel runs here, so these tests need no GPU."""
+
+import ctypes as C
+
+import pytest
+
+from paper_1708_02983_b200 import _lib
+from paper_1708_02983_b200.errors import InputError, ShapeError
+
+NULL = None
+FAKE = 0x1000  # never dereferenced: validation fails or the size is zero first
+
+
+def call(name, *args):
+    _lib.call(name, *args)
+
+
+def test_shape_errors_carry_messages():
+    with pytest.raises(ShapeError, match="negative"):
+        call("esgd_worker_step_f32", FAKE, FAKE, FAKE, FAKE, -1, 0.1, 0.01, NULL)
+    with pytest.raises(ShapeError, match="pitch"):
+        call("esgd_sync_update_f32", FAKE, 10, FAKE, 10, 2, FAKE, FAKE, 100, 0.1, 0.01, 2, NULL)
+    with pytest.raises(ShapeError):
+        call("esgd_replica_tree_sum_f32", FAKE, FAKE, 10, 2, 100, NULL)
+    with pytest.raises(ShapeError):
+        call("esgd_transpose_f32", FAKE, 1, 0, FAKE, 1, 0, -3, 4, 1, NULL)
+
+
+def test_input_errors():
+    with pytest.raises(InputError, match="num_workers"):
+        call("esgd_sync_update_f32", FAKE, 64, FAKE, 64, 1, FAKE, FAKE, 64, 0.1, 0.01, 0, NULL)
+    with pytest.raises(InputError):  # null buffers with work to do
+        call("esgd_worker_step_f32", NULL, FAKE, FAKE, FAKE, 10, 0.1, 0.01, NULL)
+    with pytest.raises(InputError, match="batch size"):
+        call("esgd_sample_batch_f32", FAKE, 0, FAKE, NULL, FAKE, FAKE, 10, 4, FAKE, FAKE, 11, 1, NULL)
+    with pytest.raises(InputError):
+        call("esgd_randint_u64", FAKE, 1, 0, 4, 0, NULL)  # upper bound 0
+    with pytest.raises(InputError):
+        call("esgd_tc_gemm_f32", NULL, NULL)
+
+
+def test_zero_length_is_a_noop():
+    # n = 0: OK without any pointer or launch
+    call("esgd_worker_step_f32", NULL, NULL, NULL, NULL, 0, 0.1, 0.01, NULL)
+    call("esgd_sync_update_f32", NULL, 0, NULL, 0, 1, NULL, NULL, 0, 0.1, 0.01, 1, NULL)
+    call("esgd_measgd_update_f32", NULL, NULL, NULL, NULL, 0, 0.1, 0.9, 0.01, NULL)
+    call("esgd_hogwild_apply_f32", NULL, NULL, NULL, 0, 0.01, NULL)
+
+
+def test_tc_gemm_descriptor_validation():
+    d = _lib.TcGemmDesc(64, 64, 32, 1, FAKE, 30, 0, FAKE, 32, 0, FAKE, 64, 1, 0, NULL, 0, NULL, 0, 0, 0, 0, 0, 3,
+                        0, 0, NULL, 0)
+    with pytest.raises(ShapeError, match="lda"):  # lda < k and not a multiple of 4
+        _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
+    d.lda, d.precision = 32, 2
+    with pytest.raises(InputError, match="precision"):
+        _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
+    d.precision, d.act = 3, 7
+    with pytest.raises(InputError, match="activation"):
+        _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
+    d.act, d.m = 0, 0  # empty output: no-op
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
