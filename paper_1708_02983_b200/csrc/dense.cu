@@ -5,6 +5,8 @@
 // column sums (bias gradients, network.py:195).
 #include "esgd_common.cuh"
 
+#include <stdlib.h>
+
 #include <math.h>
 
 namespace esgd {
@@ -345,8 +347,12 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
   ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
   ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
   // 32x32 tiles when 64x64 tiles cannot fill the machine (skinny outputs)
+  // tuning knobs (read once): ESGD_FFMA_TILE = 32 / 64 forces the tile,
+  // ESGD_FFMA_MAXSPLIT caps the K split
+  static const int force_tile = getenv("ESGD_FFMA_TILE") ? atoi(getenv("ESGD_FFMA_TILE")) : 0;
+  static const int max_split = getenv("ESGD_FFMA_MAXSPLIT") ? atoi(getenv("ESGD_FFMA_MAXSPLIT")) : 128;
   const int t64 = ((d->n + 63) / 64) * ((d->m + 63) / 64);
-  const bool small = t64 < kNumSMs;
+  const bool small = force_tile ? force_tile == 32 : t64 < kNumSMs;
   const int TM = small ? 32 : 64, TN = TM;
   // the K split depends on the per-entry problem only (never on `batch`):
   // replicas compute bit-identical results whatever the launch groups them with
@@ -357,7 +363,8 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
     int want = (2 * kNumSMs + tiles - 1) / tiles;
     int maxs = d->k / (4 * BK);
     splits = want < maxs ? want : maxs;
-    if (splits > 128) splits = 128;
+    if (splits > max_split) splits = max_split;
+    if (splits < 1) splits = 1;
     if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats || (int64_t)d->batch * splits > 65535)
       splits = 1;
   }
