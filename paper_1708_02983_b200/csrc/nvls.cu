@@ -87,10 +87,14 @@ __global__ void __launch_bounds__(256) k_sync_update_nvls(float* W, int64_t ldw,
 
 // Center slice only (the overlapped variant): runs on a side stream
 // concurrently with the round's forward/backward, which never touches S or C.
-// Four float4 NVLS loads in flight per thread hide the NVLink round trip.
-__global__ void __launch_bounds__(256) k_center_nvls(const float* __restrict__ C_old, const float* S_mc,
-                                                     float* C_new_mc, int64_t lo, int64_t hi, float er, float p) {
-  constexpr int U = 4;
+// Sized to fit NEXT TO a persistent tcgen05 GEMM CTA on the same SM (that
+// kernel leaves ~8K registers and 2 KB of shared memory free): 128 threads x
+// <= 40 registers, no shared memory — so the GEMM's CTAs are never held back
+// by the collective (measured: a 256 x 58-register version delayed them).
+// Two float4 NVLS loads in flight per thread hide the NVLink round trip.
+__global__ void __launch_bounds__(128, 12) k_center_nvls(const float* __restrict__ C_old, const float* S_mc,
+                                                         float* C_new_mc, int64_t lo, int64_t hi, float er, float p) {
+  constexpr int U = 2;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = lo + tid; i0 < hi; i0 += U * nth) {
     float4 s[U], c[U];
@@ -235,7 +239,7 @@ extern "C" int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, 
   const int64_t nv = n4 / 4, per = (nv + world - 1) / world;
   const int64_t lo = std::min<int64_t>(nv, per * rank), hi = std::min<int64_t>(nv, lo + per);
   const int grid = ctas > 0 ? ctas : kNumSMs;
-  k_center_nvls<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(C_old, S_mc, C_new_mc, lo, hi, etarho,
+  k_center_nvls<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(C_old, S_mc, C_new_mc, lo, hi, etarho,
                                                                           (float)num_workers);
   return check_launch("esgd_center_step_nvls_f32");
 }

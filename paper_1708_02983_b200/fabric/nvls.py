@@ -77,8 +77,8 @@ class NvlsRound:
         of C[p^1] = center step of C[p] with the all-rank sum of S[p]
         (NVSwitch ld_reduce), broadcast to every rank (multicast store)."""
         p = parity & 1
-        if ctas is None:  # few CTAs: the NVLink traffic hides behind the backward anyway
-            ctas = int(os.environ.get("ESGD_NVLS_CTAS", "64"))
+        if ctas is None:  # one small CTA per SM, co-resident with the GEMM CTAs
+            ctas = int(os.environ.get("ESGD_NVLS_CTAS", "148"))
         self.barrier(stream)
         _lib.call("esgd_center_step_nvls_f32", self.C[p].data_ptr(), self.S_mc[p], self.C_mc[p ^ 1], self.ld,
                   self.world, self.rank, hyper.etarho32, int(num_workers), ctas, stream_ptr(stream))
