@@ -64,10 +64,15 @@ struct Cfg {
   static constexpr int kOffBLo = kOffB + kTileBytesB;
   static constexpr int kStageBytes = kTileBytesA + kTileBytesB * (SPLIT ? 2 : 1);
   static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
-  static constexpr int kACol0 = 2 * BN;  // TMEM columns of the A regions (64 per slot: hi 32 | lo 32)
+#ifndef ESGD_ACC_BUFS128
+#define ESGD_ACC_BUFS128 2
+#endif
+  // TMEM accumulator buffers (chunks in flight between the MMA and the drain)
+  static constexpr int kAccBufs = (BN == 128 && SPLIT) ? ESGD_ACC_BUFS128 : 2;
+  static constexpr int kACol0 = kAccBufs * BN;  // TMEM columns of the A regions (64 per slot: hi 32 | lo 32)
   // TMEM A slots (a ring of its own): as many as the 512 columns leave next to
   // the two BN-wide accumulators — 4 at BN <= 128, 2 at BN = 192
-  static constexpr int kASlots = SPLIT ? ((512 - 2 * BN) / 64 < kStages ? (512 - 2 * BN) / 64 : kStages) : 1;
+  static constexpr int kASlots = SPLIT ? ((512 - kACol0) / 64 < kStages ? (512 - kACol0) / 64 : kStages) : 1;
   static constexpr int kTmemCols = SPLIT ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
   static_assert(!SPLIT || (kASlots >= 2 && kACol0 + 64 * kASlots <= 512), "TMEM budget");
   static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
@@ -412,10 +417,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 32 KB, 1024-aligned
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + C::kStageOutBytes);
   // bars: full[S], split[S], empty[S], acc_full[2], acc_empty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 2 * C::kAccBufs);
   const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
                  empty0 = smem_u32(bars + 2 * C::kStages), afull0 = smem_u32(bars + 3 * C::kStages),
-                 aempty0 = afull0 + 16;
+                 aempty0 = afull0 + 8 * C::kAccBufs;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (ep.n + BN - 1) / BN, ntm = (ep.m + BM - 1) / BM;
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(split0 + 8 * s, 4);  // one arrive per split warp
       mbar_init(empty0 + 8 * s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::kAccBufs; ++b) {
       mbar_init(afull0 + 8 * b, 1);   // tcgen05.commit
       mbar_init(aempty0 + 8 * b, kDrainWarps);  // one arrive per drain warp
     }
@@ -469,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
         for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
-          const int buf = c & 1;
-          if (c >= 2) mbar_wait(aempty0 + 8 * buf, ((c >> 1) - 1) & 1);
+          const int buf = c % C::kAccBufs;
+          if (c >= (uint32_t)C::kAccBufs) mbar_wait(aempty0 + 8 * buf, ((c / C::kAccBufs) - 1) & 1);
           tc_fence_after();
           const uint32_t acc = tmem + buf * BN;
           const int kend = min(w.nkb, kc + kChunkKB);
@@ -578,8 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < HB; ++j) racc[j] = 0.f;
       for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
-        const int buf = c & 1;
-        mbar_wait(afull0 + 8 * buf, (c >> 1) & 1);
+        const int buf = c % C::kAccBufs;
+        mbar_wait(afull0 + 8 * buf, (c / C::kAccBufs) & 1);
         tc_fence_after();
         if (HB <= 64) {
 #pragma unroll
