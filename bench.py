@@ -341,22 +341,20 @@ def launches_per_step(eng) -> int:
 
 
 def run_e2e(args, spec, train, cfg, world):
-    """Public API, host data: run_trainer with the problem's host-staged batches."""
+    """End to end through the package's host-fed runner (trainers.HostFedRun):
+    the dataset in pinned host memory, every round's batch H2D inside the
+    round, the round's loss read back to the host after every round."""
     import torch
 
-    from paper_1708_02983_b200.trainers import NetworkProblem
-    from paper_1708_02983_b200.trainers.synchronous import SyncEngine
+    from paper_1708_02983_b200.trainers import HostFedRun, NetworkProblem
 
-    prob = NetworkProblem(spec, train, None)
-    eng = SyncEngine(cfg, prob, use_graph=False, profile_rounds=0)
-    # big rows: per-row DMA from the pinned dataset; small rows: host gather + one H2D
-    stager = DmaStager(prob, eng) if spec.input_dim * 4 >= 65536 else ZeroCopyStager(prob, eng)
+    run = HostFedRun(cfg, NetworkProblem(spec, train, None))
     for _ in range(max(1, args.warmup)):
-        stager.step()
+        run.step()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        stager.step()
+        run.step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     if world > 1:
@@ -366,258 +364,7 @@ def run_e2e(args, spec, train, cfg, world):
         dt = float(t.item())
     b = cfg.batch_size
     return {"value": round(args.steps * cfg.cluster.workers * b / dt, 1), "unit": "samples/s",
-            "h2d_bytes_per_step": stager.h2d_bytes, "d2h_bytes_per_step": stager.d2h_bytes,
-            "path": ("host SplitMix64 sampling -> per-row DMA from the pinned dataset (copy stream, overlapped) -> "
-                     "(graph: round, loss D2H) -> sync" if isinstance(stager, DmaStager) else
-                     "(graph: device SplitMix64 sampling reading the rows from the pinned host dataset over PCIe, "
-                     "round, loss D2H) -> sync")}
-
-
-class HostStager:
-    """Host data path of the e2e measurement, pipelined like a data loader:
-    each round's batches are drawn on the host with the workers' SplitMix64
-    streams and gathered (thread pool) into one of two pinned buffers while
-    the device runs the previous round; one CUDA graph per buffer does the
-    H2D copy, the round and the D2H of the round's mean loss, which is read
-    back after every round."""
-
-    def __init__(self, prob, eng, threads: int = 8):
-        import concurrent.futures as cf
-
-        import torch
-
-        from paper_1708_02983_b200.rng import CounterRng, stream_seed
-
-        self.prob, self.eng = prob, eng
-        net = eng.plan.net
-        self.net = net
-        b, nrep, d = net.b, net.nrep, net.d_in
-        self.X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
-        self.Y = prob.train.labels.astype(np.int32)
-        self.rngs = [CounterRng(stream_seed(eng.cfg.seed, w)) for w in range(eng.first, eng.first + nrep)]
-        self.hx = [torch.empty((nrep, b * d), dtype=torch.float32).pin_memory() for _ in range(2)]
-        self.hy = [torch.empty((nrep, b), dtype=torch.int32).pin_memory() for _ in range(2)]
-        self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
-        self.h2d_bytes = self.hx[0].numel() * 4 + self.hy[0].numel() * 4
-        self.d2h_bytes = nrep * 4
-        self.graphs = [None, None]
-        self.pool = cf.ThreadPoolExecutor(max_workers=threads)
-        self.cur = 0
-        self.pending = self.pool.submit(self._stage_host, 0)
-        self.inflight = False
-
-    def _gather(self, dst, idx):
-        np.take(self.X, idx, axis=0, out=dst)
-
-    def _stage_host(self, k):
-        hx, hy = self.hx[k].numpy(), self.hy[k].numpy()
-        net = self.net
-        jobs = []
-        for r, rng in enumerate(self.rngs):
-            idx = rng.randint_block(net.b, self.X.shape[0])
-            hy[r] = self.Y[idx]
-            rows = hx[r].reshape(net.b, net.d_in)
-            step = max(1, net.b // 8)
-            for lo in range(0, net.b, step):  # big rows: gather in parallel chunks
-                jobs.append((rows[lo:lo + step], idx[lo:lo + step]))
-        if len(jobs) > 1 and self.X.shape[1] >= 4096:
-            list(self.pool.map(lambda j: self._gather(*j), jobs))
-        else:
-            for dst, idx in jobs:
-                self._gather(dst, idx)
-
-    def _device_round(self, k):
-        import torch
-
-        from paper_1708_02983_b200.device import stream_ptr
-
-        eng, net = self.eng, self.net
-        net.x.copy_(self.hx[k], non_blocking=True)
-        net.y.copy_(self.hy[k], non_blocking=True)
-        cs = torch.cuda.current_stream()
-        eng.comm.wait_stream(cs)
-        with torch.cuda.stream(eng.comm):
-            eng._sum(eng.comm)
-        net.gradient(eng.G, eng.W, stream_ptr(cs))
-        cs.wait_stream(eng.comm)
-        eng._update(cs)
-        self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
-
-    def _graph(self, k):
-        import torch
-
-        if self.graphs[k] is None:
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
-                self._device_round(k)
-            torch.cuda.current_stream().wait_stream(s)
-            self.graphs[k] = g
-        return self.graphs[k]
-
-    def step(self):
-        import torch
-
-        k = self.cur
-        self.pending.result()                                # batch k staged on the host
-        self._graph(k).replay()                              # H2D + round + loss D2H (async)
-        self.eng.advance()
-        self.pending = self.pool.submit(self._stage_host, k ^ 1)  # stage the next batch meanwhile
-        torch.cuda.current_stream().synchronize()
-        self.cur = k ^ 1
-        return float(self.loss.numpy().mean())
-
-
-class DmaStager(HostStager):
-    """Host data path for big rows (ImageNet-sized): the dataset lives in
-    pinned host memory; each round's rows are drawn on the host with the
-    workers' SplitMix64 streams and copied straight to one of two device
-    batch buffers by DMA (esgd_gather_rows_h2d: one cudaMemcpyAsync per row
-    on a copy stream — no host-side gather, no SMs), overlapped with the
-    previous round; one CUDA graph per buffer runs the round and the D2H of
-    the round's mean loss, which is read back after every round."""
-
-    def __init__(self, prob, eng):
-        import torch
-
-        from paper_1708_02983_b200.rng import CounterRng, stream_seed
-
-        self.prob, self.eng = prob, eng
-        net = eng.plan.net
-        self.net = net
-        b, nrep, d = net.b, net.nrep, net.d_in
-        X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
-        self.n, self.d = X.shape
-        self.Xp = torch.from_numpy(X).pin_memory()  # setup, outside the timed region
-        self.Y = prob.train.labels.astype(np.int32)
-        self.rngs = [CounterRng(stream_seed(eng.cfg.seed, w)) for w in range(eng.first, eng.first + nrep)]
-        self.xb = [torch.empty((nrep, b * d), dtype=torch.float32, device="cuda") for _ in range(2)]
-        self.yb = [torch.empty((nrep, b), dtype=torch.int32, device="cuda") for _ in range(2)]
-        self.hy = [torch.empty((nrep, b), dtype=torch.int32).pin_memory() for _ in range(2)]
-        self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
-        self.h2d_bytes = nrep * b * d * 4 + nrep * b * 4
-        self.d2h_bytes = nrep * 4
-        self.graphs = [None, None]
-        self.copy = torch.cuda.Stream()
-        self.ev = [torch.cuda.Event(), torch.cuda.Event()]
-        self.x0, self.y0 = net.x, net.y
-        self.cur = 0
-        self._load(0)
-
-    def _load(self, k):
-        import torch
-
-        from paper_1708_02983_b200 import _lib
-        from paper_1708_02983_b200.device import stream_ptr
-
-        lib = _lib.load()
-        net, hy = self.net, self.hy[k].numpy()
-        for r, rng in enumerate(self.rngs):
-            idx = np.ascontiguousarray(rng.randint_block(net.b, self.n), dtype=np.int64)
-            hy[r] = self.Y[idx]
-            _lib.check(lib.esgd_gather_rows_h2d(self.xb[k][r].data_ptr(), self.d * 4, self.Xp.data_ptr(),
-                                                self.d * 4, idx.ctypes.data, net.b, self.d * 4, self.n,
-                                                stream_ptr(self.copy)), "gather_rows_h2d")
-        with torch.cuda.stream(self.copy):
-            self.yb[k].copy_(self.hy[k], non_blocking=True)
-        self.ev[k].record(self.copy)
-
-    def _device_round(self, k):
-        import torch
-
-        from paper_1708_02983_b200.device import stream_ptr
-
-        eng, net = self.eng, self.net
-        cs = torch.cuda.current_stream()
-        eng.comm.wait_stream(cs)
-        with torch.cuda.stream(eng.comm):
-            eng._sum(eng.comm)
-        net.gradient(eng.G, eng.W, stream_ptr(cs))
-        cs.wait_stream(eng.comm)
-        eng._update(cs)
-        self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
-
-    def _graph(self, k):
-        # the round of buffer k reads xb[k] / yb[k] directly (captured pointers)
-        self.net.x, self.net.y = self.xb[k], self.yb[k]
-        try:
-            return super()._graph(k)
-        finally:
-            self.net.x, self.net.y = self.x0, self.y0
-
-    def step(self):
-        import torch
-
-        k = self.cur
-        cs = torch.cuda.current_stream()
-        cs.wait_event(self.ev[k])      # batch k on the device
-        self._graph(k).replay()        # round + loss D2H (async)
-        self.eng.advance()
-        self._load(k ^ 1)              # next batch by DMA, concurrent with round k
-        cs.synchronize()
-        self.cur = k ^ 1
-        return float(self.loss.numpy().mean())
-
-
-class ZeroCopyStager(HostStager):
-    """Host data path for small rows (MNIST-sized): the dataset lives in
-    pinned host memory and the round's sampling kernel (esgd_sample_batch_f32,
-    the workers' SplitMix64 streams on the device) reads the drawn rows
-    straight from it over PCIe (mapped pinned memory) — each round's inputs
-    cross host->device inside the round's CUDA graph, with no per-round host
-    gather or copy call; the graph also does the D2H of the round's mean
-    loss, which is read back after every round."""
-
-    def __init__(self, prob, eng):
-        import torch
-
-        self.prob, self.eng = prob, eng
-        net = eng.plan.net
-        self.net, self.plan = net, eng.plan
-        b, nrep, d = net.b, net.nrep, net.d_in
-        X = np.ascontiguousarray(prob.train.samples, dtype=np.float32)
-        self.n, self.d = X.shape
-        self.Xp = torch.from_numpy(X).pin_memory()
-        self.Yp = torch.from_numpy(prob.train.labels.astype(np.int32)).pin_memory()
-        self.loss = torch.empty(nrep, dtype=torch.float32).pin_memory()
-        self.h2d_bytes = nrep * b * d * 4 + nrep * b * 4
-        self.d2h_bytes = nrep * 4
-        self.graphs = [None, None]
-
-    def _device_round(self, k):
-        import torch
-
-        from paper_1708_02983_b200 import _lib
-        from paper_1708_02983_b200.device import stream_ptr
-
-        eng, net, plan = self.eng, self.net, self.plan
-        cs = torch.cuda.current_stream()
-        _lib.check(_lib.load().esgd_sample_batch_f32(
-            net.x.data_ptr(), net.x.stride(0), net.y.data_ptr(), None, self.Xp.data_ptr(), self.Yp.data_ptr(),
-            self.n, self.d, plan.rng.state.data_ptr(), plan.rng.ticket.data_ptr(), net.b, net.nrep,
-            stream_ptr(cs)), "sample_batch (pinned host rows)")
-        eng.comm.wait_stream(cs)
-        with torch.cuda.stream(eng.comm):
-            eng._sum(eng.comm)
-        net.gradient(eng.G, eng.W, stream_ptr(cs))
-        cs.wait_stream(eng.comm)
-        eng._update(cs)
-        self.loss.copy_(net.row_loss[:, :net.b].mean(dim=1), non_blocking=True)
-
-    def step(self):
-        import torch
-
-        k = self.eng.parity if self.eng.nvls is not None else 0
-        rng = self.plan.rng.state
-        if self.graphs[k] is None:  # capture does not run the sampling kernel: keep the RNG as is
-            before = rng.clone()
-            self._graph(k)
-            rng.copy_(before)
-        self.graphs[k].replay()
-        self.eng.advance()
-        torch.cuda.current_stream().synchronize()
-        return float(self.loss.numpy().mean())
+            "h2d_bytes_per_step": run.h2d_bytes, "d2h_bytes_per_step": run.d2h_bytes, "path": run.path}
 
 
 # CPU sample batch per worker round: AlexNet's b=128 round is ~10 s of numpy,

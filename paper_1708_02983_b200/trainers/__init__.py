@@ -9,6 +9,7 @@ from .config import METHOD_SCHEDULERS, METHODS, TrainerConfig, make_config
 from .problems import NetworkProblem, QuadraticProblem, ZeroGradientProblem
 from .records import RunRecord, weights_digest
 from .synchronous import SYNC_METHODS, SyncEngine, run_synchronous
+from .hostfeed import HostFedRun
 
 ASYNC_METHODS = ("async-sgd", "async-easgd", "async-msgd", "async-measgd")
 HOGWILD_METHODS = ("hogwild-sgd", "hogwild-easgd")
@@ -37,6 +38,7 @@ def run_trainer(cfg: TrainerConfig, problem, cost_model: CostModel | None = None
 
 
 __all__ = [
+    "HostFedRun",
     "ASYNC_METHODS",
     "HOGWILD_METHODS",
     "METHODS",
