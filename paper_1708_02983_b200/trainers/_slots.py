@@ -5,6 +5,8 @@ different devices; the center lives on the master device."""
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -60,7 +62,9 @@ class WorkerSlot:
         try:
             with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
                 self.plan.gradient(self.G, self.W, stream_ptr(side))
-        except Exception:  # capture unsupported: stay eager
+        except Exception as exc:  # capture unsupported: stay eager
+            warnings.warn(f"worker {self.wid}: CUDA graph capture failed ({exc}); running eagerly",
+                          RuntimeWarning, stacklevel=2)
             torch.cuda.synchronize(self.device)
             return
         self.stream.wait_stream(side)

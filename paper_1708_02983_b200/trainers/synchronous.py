@@ -25,6 +25,7 @@ B200 mapping:
 from __future__ import annotations
 
 import time
+import warnings
 
 import numpy as np
 import torch
@@ -101,7 +102,9 @@ class SyncEngine:
             if self.fused_sum and nvls_wanted():
                 try:
                     self.nvls = NvlsRound(ld, dev)
-                except Exception:  # no multicast object support: NCCL path
+                except Exception as exc:  # no multicast object support: NCCL path
+                    warnings.warn(f"NVLS multicast unavailable ({exc}); using one NCCL allreduce per round",
+                                  RuntimeWarning, stacklevel=2)
                     self.nvls = None
                     torch.cuda.synchronize()
             if self.nvls is not None:
@@ -211,7 +214,9 @@ class SyncEngine:
         if self.use_graph and self.profiled >= self.profile_rounds:
             try:
                 self._capture()
-            except Exception:  # capture unsupported here (e.g. NCCL): stay eager
+            except Exception as exc:  # capture unsupported here: stay eager
+                warnings.warn(f"CUDA graph capture of the round failed ({exc}); running eagerly",
+                              RuntimeWarning, stacklevel=2)
                 self.use_graph = False
                 torch.cuda.synchronize()
             if self.graphs[k] is not None:
