@@ -407,6 +407,20 @@ __device__ __forceinline__ void general_quarter(const Epi& ep, uint32_t sb, int 
   }
 }
 
+#ifdef ESGD_TRACE
+// timing probe build only: clock64 stamps of CTA 0's roles (tools/trace_gemm.py)
+constexpr int kTraceN = 4096;
+__device__ unsigned long long g_trace[8][kTraceN];
+#define TRACE(row, idx)                                                          \
+  do {                                                                           \
+    if (blockIdx.x == 0 && (idx) < kTraceN) g_trace[row][idx] = clock64();       \
+  } while (0)
+#else
+#define TRACE(row, idx) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int BN, bool SPLIT, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -459,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
           if (g >= (uint32_t)C::kStages) mbar_wait(empty0 + 8 * s, ((g / C::kStages) - 1) & 1);
+          TRACE(0, g);
           uint8_t* st = smem + s * C::kStageBytes;
           mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
           load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
@@ -476,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
           const int buf = c % C::kAccBufs;
           if (c >= (uint32_t)C::kAccBufs) mbar_wait(aempty0 + 8 * buf, ((c / C::kAccBufs) - 1) & 1);
+          TRACE(2, c);
           tc_fence_after();
           const uint32_t acc = tmem + buf * BN;
           const int kend = min(w.nkb, kc + kChunkKB);
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (g / C::kStages) & 1;
             if (SPLIT) mbar_wait(split0 + 8 * s, ph);
             else mbar_wait(full0 + 8 * s, ph);
+            TRACE(1, g);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + s * C::kStageBytes);
 #pragma unroll
@@ -520,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
+          if (warp == 2 && lane == 0) TRACE(3, g);
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           uint32_t hi[32], lo[32];
           if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
@@ -562,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(split0 + 8 * s);
+          if (warp == 2 && lane == 0) TRACE(4, g);
         }
       }
     }
@@ -585,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
         const int buf = c % C::kAccBufs;
         mbar_wait(afull0 + 8 * buf, (c / C::kAccBufs) & 1);
+        if (warp == 6 && lane == 0) TRACE(5, c);
         tc_fence_after();
         if (HB <= 64) {
 #pragma unroll
@@ -607,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
+        if (warp == 6 && lane == 0) TRACE(6, c);
       }
       const int row = w.m0 + q * 32 + lane;
       const int n0 = w.n0 + h * HB;  // first column of this warp's half
@@ -869,3 +890,9 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
   if (bn == 192) return tc::launch_major<192, true>(use, st);
   return split ? tc::launch_major<128, true>(use, st) : tc::launch_major<128, false>(use, st);
 }
+
+#ifdef ESGD_TRACE
+extern "C" int esgd_trace_copy(void* dst) {
+  return cudaMemcpyFromSymbol(dst, esgd::tc::g_trace, sizeof(esgd::tc::g_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
