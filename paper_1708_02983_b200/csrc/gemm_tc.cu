@@ -407,8 +407,12 @@ __device__ __forceinline__ void general_quarter(const Epi& ep, uint32_t sb, int 
   }
 }
 
+// Diagnostic builds only (tools/build_variant.sh; never in libesgd.so):
+// ESGD_TRACE stamps CTA 0's role timeline; ESGD_X_{NOTMA,NOAST,NOSPLITB,
+// NODRAIN,NOEPI} switch one role's work off (wrong results, timing only) to
+// attribute the gap between the MMA issue rate and the tensor-core floor.
 #ifdef ESGD_TRACE
-// timing probe build only: clock64 stamps of CTA 0's roles (tools/trace_gemm.py)
+// clock64 stamps of CTA 0's roles (tools/trace_gemm.py)
 constexpr int kTraceN = 4096;
 __device__ unsigned long long g_trace[8][kTraceN];
 #define TRACE(row, idx)                                                          \
@@ -475,6 +479,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g >= (uint32_t)C::kStages) mbar_wait(empty0 + 8 * s, ((g / C::kStages) - 1) & 1);
           TRACE(0, g);
           uint8_t* st = smem + s * C::kStageBytes;
+#ifdef ESGD_X_NOTMA
+          if (g >= (uint32_t)C::kStages) { mbar_arrive(full0 + 8 * s); continue; }
+#endif
           mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
           load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
           load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb, w.n0, w.z);
@@ -572,9 +579,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + C::kACol0 + (g % C::kASlots) * 64;
+#ifndef ESGD_X_NOAST
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
+#endif
+#ifndef ESGD_X_NOSPLITB
           split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
+#endif
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_before();
@@ -606,6 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(afull0 + 8 * buf, (c / C::kAccBufs) & 1);
         if (warp == 6 && lane == 0) TRACE(5, c);
         tc_fence_after();
+#ifndef ESGD_X_NODRAIN
         if (HB <= 64) {
 #pragma unroll
           for (int c0 = 0; c0 < HB; c0 += 32) {
@@ -624,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 16; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], v[j]);
           }
         }
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
@@ -631,7 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int row = w.m0 + q * 32 + lane;
       const int n0 = w.n0 + h * HB;  // first column of this warp's half
-      if (ep.splits > 1) {  // raw partial of this K slice; k_tc_reduce applies the epilogue
+#ifdef ESGD_X_NOEPI
+      if (row == -1) {
+#else
+      if (ep.splits > 1) {
+#endif  // raw partial of this K slice; k_tc_reduce applies the epilogue
         if (row < ep.m) {
           float* P = ep.ws + ((int64_t)w.z * ep.splits + w.slice) * ep.m * ep.n + (int64_t)row * ep.n;
 #pragma unroll
