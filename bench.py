@@ -276,8 +276,10 @@ def run_device(args):
                 "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
                 "algorithmic_flops_per_launch": fl,
                 "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)"}
-    else:
-        roof = roof_upd
+    else:  # no GEMM reaches the tensor-core threshold (LeNet): the round is launch/latency-bound
+        roof = dict(roof_upd, note="no tcgen05 GEMM in this round (all GEMMs below the tensor-core "
+                    "threshold run on the FFMA kernel); the round is launch/latency-bound "
+                    "(profiles/r01_launches_lenet.md), the update kernel is the one HBM-bound launch")
 
     # e2e: run_trainer's host data path (pinned batch H2D + loss D2H every round)
     e2e = run_e2e(args, spec, train, cfg, world) if not args.no_e2e else None
