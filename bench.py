@@ -81,13 +81,47 @@ def make_data(model: str, spec, seed: int = 0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons during the timed region: NVML every 10 ms
+    (the device matched by PCI bus id), nvidia-smi every 0.2 s if NVML is
+    unavailable."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index, self.rows, self._stop = index, [], threading.Event()
         self.th = threading.Thread(target=self._run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            try:
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                try:
+                    h = N.nvmlDeviceGetHandleByPciBusId(bus)
+                except Exception:
+                    h = N.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(index)
+            self.nvml = (N, h, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        except Exception:
+            self.nvml = None
 
     def _run(self):
+        if self.nvml is not None:
+            N, h, mx = self.nvml
+            while not self._stop.is_set():
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                    bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append([str(sm), str(mx)] + [
+                        "Active" if bits & m else "Not Active" for m in (0x8, 0x40, 0x20, 0x4)])
+                except Exception:
+                    pass
+                self._stop.wait(0.01)
+            return
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -119,7 +153,7 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
                           and "Not" not in r[2 + i]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_setup(n_gpus: int):
