@@ -36,6 +36,8 @@ extern "C" {
 #define ESGD_ACT_SIGMOID 3
 
 typedef void* esgd_stream_t;
+typedef void* esgd_comm_t; /* an NCCL communicator (ncclComm_t) */
+#define ESGD_NCCL_ID_BYTES 128
 
 /* ---- library ----------------------------------------------------------- */
 const char* esgd_last_error(void);
@@ -102,6 +104,21 @@ int esgd_worker_step_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg,
  * zero-initialised); epoch = this rank's device counter (graph-replayable). */
 int esgd_nvls_barrier(int32_t* const* peer_flags, int32_t world, int32_t rank, int32_t* epoch,
                       esgd_stream_t stream);
+
+/* ---- collective (no torch.distributed) ----------------------------------- */
+/* The cross-GPU replica sum of the Sync round as an in-place NCCL allreduce,
+ * for hosts that drive libesgd directly (SURVEY.md §8(b) esgd_nccl_init_all /
+ * esgd_allreduce_sum_f32 / esgd_nccl_destroy; replaces the reference's
+ * tree_sum over workers, fabric/collectives.py:18-32, across processes). NCCL
+ * is dlopen'ed (libnccl.so.2); without it these return ESGD_ERR_UNSUPPORTED.
+ * Rank 0 creates the id, the host ships its 128 bytes to every rank, each
+ * rank (with its GPU current) calls esgd_nccl_init. The sum order is NCCL's
+ * (bitwise equal to the binomial tree at world = 2).                       */
+int esgd_nccl_available(void);
+int esgd_nccl_unique_id(void* id_out /* ESGD_NCCL_ID_BYTES */);
+int esgd_nccl_init(esgd_comm_t* comm, const void* id, int32_t world, int32_t rank);
+int esgd_allreduce_sum_f32(esgd_comm_t comm, float* buf, int64_t n, esgd_stream_t stream);
+int esgd_nccl_destroy(esgd_comm_t comm);
 
 /* measgd_worker_step, updates.py:134-140 (in place):
  *   v = mu*v - eta*g;  w = (w + v) - etarho*(w - c).  24 B/param.          */

@@ -78,6 +78,11 @@ _SIGS = {
     "esgd_sync_update_nvls_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, vp, vp, i64, i32, i32, f32, f32, i32,
                                             vp]),
     "esgd_nvls_barrier": (C.c_int, [vp, i32, i32, vp, vp]),
+    "esgd_nccl_available": (C.c_int, []),
+    "esgd_nccl_unique_id": (C.c_int, [vp]),
+    "esgd_nccl_init": (C.c_int, [vp, vp, i32, i32]),
+    "esgd_allreduce_sum_f32": (C.c_int, [vp, vp, i64, vp]),
+    "esgd_nccl_destroy": (C.c_int, [vp]),
     "esgd_center_step_nvls_f32": (C.c_int, [vp, vp, vp, i64, i32, i32, f32, i32, i32, vp]),
     "esgd_worker_step_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, f32, f32, vp]),
     "esgd_sync_update_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, vp, i64, f32, f32, i32, vp]),

@@ -52,6 +52,42 @@ def local_workers(workers: int, world_size: int, rank: int) -> range:
     return range(rank * per, (rank + 1) * per)
 
 
+class CabiComm:
+    """The packed-buffer allreduce through libesgd's own NCCL communicator
+    (esgd_nccl_init / esgd_allreduce_sum_f32, include/esgd.h) — the path a
+    host without torch.distributed uses; here torch.distributed only ships
+    the 128-byte id from rank 0. Selected with ESGD_COLLECTIVE=cabi."""
+
+    def __init__(self, device, group=None):
+        import ctypes as C
+
+        w, r = world()
+        if w < 2:
+            raise InputError("CabiComm needs an initialised process group of >= 2 ranks")
+        lib = _lib.load()
+        if not lib.esgd_nccl_available():
+            raise InputError("libnccl.so.2 is not loadable")
+        uid = (C.c_ubyte * 128)()
+        if r == 0:
+            _lib.check(lib.esgd_nccl_unique_id(C.cast(uid, C.c_void_p)), "nccl_unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        self.comm = C.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(lib.esgd_nccl_init(C.byref(self.comm), C.cast(uid, C.c_void_p), w, r), "nccl_init")
+        self.world, self.rank = w, r
+
+    def allreduce_sum_(self, S: torch.Tensor, stream=None) -> None:
+        check_f32(S)
+        _lib.call("esgd_allreduce_sum_f32", self.comm, ptr(S), S.numel(), stream_ptr(stream))
+
+    def close(self) -> None:
+        if self.comm:
+            _lib.call("esgd_nccl_destroy", self.comm)
+            self.comm = None
+
+
 def world() -> tuple[int, int]:
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(), dist.get_rank()

@@ -24,6 +24,7 @@ B200 mapping:
 
 from __future__ import annotations
 
+import os
 import time
 import warnings
 
@@ -33,7 +34,7 @@ import torch.distributed as dist
 
 from ..device import require_cuda, round_up, stream_ptr
 from ..errors import InputError
-from ..fabric.collectives import allreduce_sum_, local_workers, replica_sum_, world
+from ..fabric.collectives import CabiComm, allreduce_sum_, local_workers, replica_sum_, world
 from ..fabric.nvls import NvlsRound, nvls_fused_single_kernel, nvls_wanted
 from ..fabric.engine import CATEGORIES
 from ..rng import stream_seed
@@ -112,10 +113,17 @@ class SyncEngine:
                 self.nvls.S[0].copy_(self.S)
                 self.C, self.S = self.nvls.C[0], self.nvls.S[0]
                 torch.cuda.synchronize()
+        # ESGD_COLLECTIVE=cabi: the allreduce through libesgd's own NCCL
+        # communicator (the C-ABI path of hosts without torch.distributed)
+        self.cabi = None
+        if self.world > 1 and self.nvls is None and os.environ.get("ESGD_COLLECTIVE") == "cabi":
+            self.cabi = CabiComm(dev)
+            torch.cuda.synchronize()
         self.graphs = [None, None]
         self.nvls_single = nvls_fused_single_kernel()
         self.collective = ("nvls-fused" if self.nvls is not None else
-                           ("nccl-allreduce" if self.world > 1 else "none"))
+                           ("nccl-cabi" if self.cabi is not None else
+                            ("nccl-allreduce" if self.world > 1 else "none")))
 
     # ---- one round ------------------------------------------------------------
     def _sum(self, stream) -> None:
@@ -124,7 +132,7 @@ class SyncEngine:
                 self.nvls.center(self.parity, self.P, self.cfg.hyper, stream)
             return
         if self.fused_sum:  # local sum already formed by the previous update
-            allreduce_sum_(self.S)
+            self._allreduce(stream)
             return
         if self.partials is not None:
             gsize = self.nrep // self.local_groups
@@ -133,7 +141,13 @@ class SyncEngine:
             replica_sum_(self.S, self.partials, self.n, stream)
         else:
             replica_sum_(self.S, self.W, self.n, stream)
-        allreduce_sum_(self.S)
+        self._allreduce(stream)
+
+    def _allreduce(self, stream) -> None:
+        if self.cabi is not None:
+            self.cabi.allreduce_sum_(self.S, stream)
+        else:
+            allreduce_sum_(self.S)  # torch.distributed, on the current stream
 
     def _gradient(self, stream) -> None:
         self.plan.gradient(self.G, self.W, stream_ptr(stream))

@@ -64,3 +64,18 @@ def test_tc_gemm_descriptor_validation():
         _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
     d.act, d.m = 0, 0  # empty output: no-op
     _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), NULL))
+
+
+def test_collective_argument_checks():
+    # include/esgd.h collective entries: validation before any NCCL call
+    with pytest.raises(ShapeError, match="negative"):
+        call("esgd_allreduce_sum_f32", NULL, FAKE, -1, NULL)
+    call("esgd_allreduce_sum_f32", NULL, NULL, 0, NULL)  # empty: no-op
+    with pytest.raises(InputError, match="null"):
+        call("esgd_allreduce_sum_f32", NULL, FAKE, 8, NULL)
+    comm = C.c_void_p()
+    uid = (C.c_ubyte * 128)()
+    with pytest.raises(InputError, match="outside world"):
+        call("esgd_nccl_init", C.byref(comm), C.cast(uid, C.c_void_p), 2, 2)
+    call("esgd_nccl_destroy", NULL)  # null communicator: no-op
+    assert _lib.load().esgd_nccl_available() in (0, 1)
