@@ -186,9 +186,13 @@ __global__ void __launch_bounds__(256) k_im2col_rows(float* __restrict__ col, in
                                                      int stride, int pad, int oh, int ow) {
   const int z = blockIdx.z;
   const int ohw = oh * ow, np = xd.n * ohw;
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  // grid x = (channel, kernel row), y = pixel block: the KS*C work items of
+  // one pixel block run back to back, so the input rows their overlapping
+  // windows share are still in L2 (x-fastest over pixels re-read the input
+  // 2.1x from DRAM, r01_ncu_conv.md)
+  const int pix = blockIdx.y * blockDim.x + threadIdx.x;
   if (pix >= np) return;
-  const int c = blockIdx.y / KS, ky = blockIdx.y - c * KS;
+  const int c = blockIdx.x / KS, ky = blockIdx.x - c * KS;
   const int img = pix / ohw, p = pix - img * ohw, oy = p / ow, ox = p - oy * ow;
   const int iy = oy * stride - pad + ky, ix0 = ox * stride - pad;
   float* cp = col + z * col_sb + (int64_t)(c * KS * KS + ky * KS) * col_sk + pix;
@@ -659,8 +663,8 @@ extern "C" int esgd_im2col_f32(float* col, int64_t col_sp, int64_t col_sk, int64
       k_im2col_sq<3><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
     else if (kh == 5)
       k_im2col_sq<5><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
-    else if (xd.c * kh <= 65535) {
-      dim3 g3((unsigned)((np + 255) / 256), (unsigned)(xd.c * kh), batch);
+    else if ((np + 255) / 256 <= 65535) {
+      dim3 g3((unsigned)(xd.c * kh), (unsigned)((np + 255) / 256), batch);
       k_im2col_rows<11><<<g3, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow);
     } else
       k_im2col_sq<11><<<g2, 256, 0, ESGD_STREAM(stream)>>>(col, col_sk, col_sb, x, xd, x_sb, stride, pad, oh, ow, gc);
