@@ -21,3 +21,15 @@ def test_reference_arm_prints_contract_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["model"] == "lenet" and d["higher_is_better"] is True
+
+
+def test_reference_arm_non_zero_rank_exits_quietly():
+    # under torchrun (N > 1) only rank 0 runs the CPU reference and prints
+    import os
+
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--model", "lenet", "--steps", "1",
+           "--warmup", "3", "--gpus", "2"]
+    env = dict(os.environ, RANK="1", LOCAL_RANK="1", WORLD_SIZE="2")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
