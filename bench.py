@@ -309,7 +309,11 @@ def run_device(args):
                 "frac": round(ach / tf32_peak, 4), "traffic": traffic(tkey, args.model),
                 "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
                 "algorithmic_flops_per_launch": fl,
-                "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)"}
+                "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)",
+                # the issue-rate floor of kind::tf32 MMAs (4096 flop/cycle/SM, measured at the
+                # floor in isolation by tools/probe_mma_rate.cu) at the max SM clock
+                "tensor_floor_tflops": round(148 * 4096 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, 1),
+                "frac_of_floor": round(ach / (148 * 4096 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12), 4)}
     else:  # no GEMM reaches the tensor-core threshold (LeNet): the round is launch/latency-bound
         roof = dict(roof_upd, note="no tcgen05 GEMM in this round (all GEMMs below the tensor-core "
                     "threshold run on the FFMA kernel); the round is launch/latency-bound "
