@@ -57,12 +57,19 @@ constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 template <int BN, bool SPLIT>
 struct Cfg {
   static constexpr int kTileBytesB = BN * BK * 4;
-  // stage layout: [A raw | B raw | B lo (3xTF32)], every tile 1024-B aligned.
+  // stage layout: [lo spill | A raw | B raw], every tile 1024-B aligned.
   // In 3xTF32 mode A never gets a lo twin in smem: the split warps write the
-  // tf32 hi/lo rows of A straight into TMEM and the MMAs read A from there.
-  static constexpr int kOffB = kTileBytesA;
-  static constexpr int kOffBLo = kOffB + kTileBytesB;
-  static constexpr int kStageBytes = kTileBytesA + kTileBytesB * (SPLIT ? 2 : 1);
+  // tf32 hi/lo rows of A straight into TMEM and the MMAs read A from there —
+  // so once they have read the A tile, B's lo twin is written over it,
+  // starting at the stage base; the spill is the part of B lo that does not
+  // fit in A's 16 KB (8 KB at BN = 192). 48 KB stages at BN = 192 give a
+  // fourth ring stage (three covered TMA latency + split + MMA per stage
+  // only partly), 32 KB at BN = 128 six.
+  static constexpr int kLoSpill = (SPLIT && kTileBytesB > kTileBytesA) ? kTileBytesB - kTileBytesA : 0;
+  static constexpr int kOffA = kLoSpill;
+  static constexpr int kOffB = kOffA + kTileBytesA;
+  static constexpr int kOffBLo = 0;
+  static constexpr int kStageBytes = kLoSpill + kTileBytesA + kTileBytesB;
   static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
 #ifndef ESGD_ACC_BUFS128
 #define ESGD_ACC_BUFS128 2
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g >= (uint32_t)C::kStages) { mbar_arrive(full0 + 8 * s); continue; }
 #endif
           mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
-          load_operand<AMN, BM>(smem_u32(st), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
+          load_operand<AMN, BM>(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
           load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb, w.n0, w.z);
         }
       }
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_tf32_ts(acc, ahi, bl, idesc_ts, 1u);
                 mma_tf32_ts(acc, ahi, bh, idesc_ts, 1u);
               } else {
-                mma_tf32(acc, op_desc<AMN>(st, kk), bh, idesc, acc0);
+                mma_tf32(acc, op_desc<AMN>(st + C::kOffA, kk), bh, idesc, acc0);
               }
             }
             mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
@@ -546,11 +553,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
           if (warp == 2 && lane == 0) TRACE(3, g);
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+          const uint32_t sa = st + C::kOffA;
           uint32_t hi[32], lo[32];
           if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const float4 x = lds4(st + r * 128 + ((c ^ (r & 7)) << 4));
+              const float4 x = lds4(sa + r * 128 + ((c ^ (r & 7)) << 4));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -560,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {  // MN-major SW128 boxes of 32(M) x 32(K): 4 KB per box, 16-B chunk (m%32)/4 ^ k%8
-            const uint32_t base = st + (r >> 5) * 4096 + ((r & 3) << 2);
+            const uint32_t base = sa + (r >> 5) * 4096 + ((r & 3) << 2);
             const int c4 = (r & 31) >> 2;
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
@@ -583,6 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
 #endif
+          // every split thread has read its A row: B lo may overwrite the tile
+          named_bar_sync(3, 128);
 #ifndef ESGD_X_NOSPLITB
           split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
 #endif
