@@ -243,9 +243,11 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
 
 // col2im for square KS x KS stride-1 kernels (AlexNet conv2-5, LeNet): the
 // KS*KS loads of a channel are issued together (predicated), then summed in
-// the same (ky, kx) order as k_col2im_t, so results are identical
+// the same (ky, kx) order as k_col2im_t, so results are identical. Capped at
+// 64 registers (4 CTAs/SM) for every KS: at 3x3 the uncapped 75 registers
+// allowed 3 (conv3-5 col2im 172 -> 156 us in total, tools/bench_conv.py).
 template <int KS>
-__global__ void __launch_bounds__(256, KS >= 5 ? 4 : 1) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+__global__ void __launch_bounds__(256, 4) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                    const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                    int pad, int oh, int ow, const float* __restrict__ mask,
                                                    int64_t mask_sb, int grp) {
