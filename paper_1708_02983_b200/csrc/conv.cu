@@ -726,8 +726,9 @@ extern "C" int esgd_rowsum_f32(float* out, int64_t out_sb, const float* x, int64
                ESGD_ERR_SHAPE, "rowsum: bad shape");
   ESGD_REQUIRE(out && x, ESGD_ERR_INPUT, "rowsum: null buffer");
   ESGD_REQUIRE(rows <= 65535 && batch <= 65535, ESGD_ERR_UNSUPPORTED, "rowsum: grid too large");
-  // ~2 CTAs per SM overall, chunks of >= 4096 elements
-  int64_t nchunk = (2 * kNumSMs + (int64_t)rows - 1) / (int64_t)rows;  // batch-independent order
+  // ~8 CTAs per SM overall (the row sums are latency-bound at fewer), chunks
+  // of >= 4096 elements
+  int64_t nchunk = (8 * kNumSMs + (int64_t)rows - 1) / (int64_t)rows;  // batch-independent order
   int64_t maxc = (cols + 4095) / 4096;
   if (nchunk > maxc) nchunk = maxc;
   if (nchunk > 64) nchunk = 64;
