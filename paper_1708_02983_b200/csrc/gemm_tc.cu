@@ -52,6 +52,10 @@ constexpr int kDrainWarps = 8;         // two per TMEM lane quadrant, each ownin
 #define ESGD_CHUNK_KB 2
 #endif
 constexpr int kChunkKB = ESGD_CHUNK_KB;
+// output-tile waves a split-K GEMM is cut into (weight gradients)
+#ifndef ESGD_SPLIT_WAVES
+#define ESGD_SPLIT_WAVES 1
+#endif
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
 template <int BN, bool SPLIT>
@@ -818,10 +822,11 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   const int tiles_z = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM);
   const int tiles = tiles_z * d->batch;
   // split K when the output tiles cannot fill the 148 SMs (weight gradients
-  // reduce over every pixel of the batch): ~2 waves, >= 2 chunks per slice
+  // reduce over every pixel of the batch): ~1 wave, >= 2 chunks per slice (2 waves: conv2.wgrad
+  // 0.30 vs 0.28 ms and a ~2% slower round - twice the partials for k_tc_reduce; 3-4 far worse)
   int splits = 1;
   if (d->ws && tiles_z < kNumSMs && nkb >= 2 * kChunkKB) {
-    splits = (2 * kNumSMs) / tiles_z;
+    splits = (ESGD_SPLIT_WAVES * kNumSMs) / tiles_z;
     splits = std::min(splits, nkb / (2 * kChunkKB));
     splits = std::min(splits, 128);
     if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats) splits = 1;  // never batch-dependent
