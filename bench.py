@@ -174,16 +174,18 @@ def dist_setup(n_gpus: int):
 def time_update_kernel(eng, reps: int = 20):
     """Live CUDA-event timing of the round's elastic-update kernel on the
     training stream with copies of the engine's buffers, L2 flushed before
-    each launch. Algorithmic bytes per param: C read+write and S read (12) +
-    12 per local replica (W read+write, G read) = 24 at nrep = 1, plus the
-    S_next write (4) when the update also forms the next round's replica sum
-    (esgd_sync_update_sum_f32, the engine's path without groups)."""
+    each launch. Algorithmic bytes per param: one worker in total (P = 1):
+    W, C read+write and G read = 20 (S = W(t), esgd_sync_update_solo_f32);
+    otherwise C read+write and S read (12) + 12 per local replica (W
+    read+write, G read), plus the S_next write (4) when the update also forms
+    the next round's replica sum (esgd_sync_update_sum_f32)."""
     import torch
 
-    from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_
+    from paper_1708_02983_b200.updates import sync_update_, sync_update_solo_, sync_update_sum_
 
     n, nrep = eng.n, eng.nrep
-    fused = getattr(eng, "fused_sum", False)
+    solo = getattr(eng, "solo", False)
+    fused = getattr(eng, "fused_sum", False) and not solo
     # work on copies so the training state is untouched
     W, G, C, S = eng.W.clone(), eng.G.clone(), eng.C.clone(), eng.S.clone()
     flush = torch.empty(int(256e6) // 4, device=W.device)
@@ -192,7 +194,9 @@ def time_update_kernel(eng, reps: int = 20):
         flush.zero_()  # evict L2 (126 MB) so the stream comes from HBM
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        if fused:
+        if solo:
+            sync_update_solo_(W, G, C, n, eng.cfg.hyper)
+        elif fused:
             sync_update_sum_(W, G, C, S, S, n, eng.P, eng.cfg.hyper)
         else:
             sync_update_(W, G, C, S, n, eng.P, eng.cfg.hyper)
@@ -200,6 +204,8 @@ def time_update_kernel(eng, reps: int = 20):
         b.synchronize()
         if i >= 3:
             times.append(a.elapsed_time(b) / 1e3)
+    if solo:
+        return n * 20, float(np.mean(times)), "esgd_sync_update_solo_f32 (k_sync_update_solo4)", "sync_update_solo"
     bytes_ = n * (12 + 12 * nrep + (4 if fused else 0))
     name = "esgd_sync_update_sum_f32 (k_sync_update_sum4)" if fused else "esgd_sync_update_f32 (k_sync_update<4>)"
     return bytes_, float(np.mean(times)), name, ("sync_update_sum" if fused else "sync_update")
@@ -364,8 +370,10 @@ def launches_per_step(eng) -> int:
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         eng.plan.gradient(G, W, stream_ptr())
         from paper_1708_02983_b200.fabric.collectives import replica_sum_
-        from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_
-        if getattr(eng, "fused_sum", False):
+        from paper_1708_02983_b200.updates import sync_update_, sync_update_solo_, sync_update_sum_
+        if getattr(eng, "solo", False):
+            sync_update_solo_(W, G, eng.C.clone(), eng.n, eng.cfg.hyper)
+        elif getattr(eng, "fused_sum", False):
             S = eng.S.clone()
             sync_update_sum_(W, G, eng.C.clone(), S, S, eng.n, eng.P, eng.cfg.hyper)
         else:
@@ -407,89 +415,165 @@ def run_e2e(args, spec, train, cfg, world):
             "h2d_bytes_per_step": run.h2d_bytes, "d2h_bytes_per_step": run.d2h_bytes, "path": run.path}
 
 
-# CPU sample batch per worker round: AlexNet's b=128 round is ~10 s of numpy,
-# so the bounded sample uses a smaller batch (samples/s is per-sample work).
-CPU_SAMPLE_B = {"lenet": 64, "cifar-quick": 64, "alexnet": 16}
-
-
 class CpuRound:
     """The CPU oracle (numpy restatement of the reference's sync round,
-    trainers/synchronous.py:57-64, P=1) on this host's cores."""
+    trainers/synchronous.py:57-64, simulated engine) on this host's cores, at
+    the native arm's per-worker batch: P workers' gradients, the tree sum and
+    the elastic worker / center steps."""
 
-    def __init__(self, args, train):
+    def __init__(self, args, train, workers: int = 1):
         from oracle import esgd_oracle as O
 
         self.O = O
         layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK, "alexnet": O.alexnet_layers(1000)}[args.model]
         self.wl = WORKLOADS[args.model]
-        self.b = min(args.batch or self.wl["b"], CPU_SAMPLE_B[args.model])
+        self.b = args.batch or self.wl["b"]
+        self.P = workers
         self.model = args.model
         self.prob = O.NetProblem(*layers, train.samples, train.labels, seed=0, dtype=np.float32)
-        self.rng = O.worker_rng(3, 0)
-        self.w = self.prob.init_weights()
-        self.c = self.w.copy()
-        self.cores = int(os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
-                         or os.cpu_count())
+        self.rngs = [O.worker_rng(3, w) for w in range(workers)]
+        w0 = self.prob.init_weights()
+        self.w = [w0.copy() for _ in range(workers)]
+        self.c = w0.copy()
+        self.cores = host_info()["threads"]
         self.round()  # warm-up (BLAS init, page faults)
 
     def round(self):
         O, wl = self.O, self.wl
-        g = self.prob.gradient(self.w, self.rng, self.b)
-        s = O.tree_sum([self.w])
-        self.w, self.c = (O.easgd_worker_step(self.w, g, self.c, wl["eta"], wl["rho"]),
-                          O.easgd_center_step_from_sum(self.c, s, 1, wl["eta"], wl["rho"]))
+        g = [self.prob.gradient(w, r, self.b) for w, r in zip(self.w, self.rngs)]
+        s = O.tree_sum(self.w)
+        self.w = [O.easgd_worker_step(w, gi, self.c, wl["eta"], wl["rho"]) for w, gi in zip(self.w, g)]
+        self.c = O.easgd_center_step_from_sum(self.c, s, self.P, wl["eta"], wl["rho"])
 
-    def sample(self, budget_s: float):
-        """As many rounds as fit in ~budget_s (at least one): (rounds, seconds)."""
+    def sample(self, budget_s: float, max_rounds: int = 1 << 30):
+        """Whole rounds until ~budget_s has passed (at least one): (rounds, seconds)."""
         rounds, t0 = 0, time.perf_counter()
         while True:
             self.round()
             rounds += 1
             elapsed = time.perf_counter() - t0
-            if elapsed >= budget_s:
+            if elapsed >= budget_s or rounds >= max_rounds:
                 return rounds, elapsed
 
     def describe(self, rounds: int) -> str:
-        return (f"{rounds} sync-easgd rounds of {self.model}, P=1, b={self.b}/round, numpy/OpenBLAS fp32 "
-                f"(oracle/esgd_oracle.py restating trainers/synchronous.py:57-64)")
+        return (f"{rounds} full sync-easgd rounds of {self.model}, P={self.P}, b={self.b}/worker (the native "
+                f"arm's per-worker batch), numpy/OpenBLAS fp32 (oracle/esgd_oracle.py restating "
+                f"trainers/synchronous.py:57-64, simulated engine)")
+
+
+def host_info() -> dict:
+    """CPU model, thread counts and the BLAS the oracle runs on."""
+    model = None
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads"), "version": i.get("version")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception:
+        pass
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+                  or len(os.sched_getaffinity(0)))
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "threads": threads, "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"), "blas": blas}
+
+
+def update_rules_gbs(n: int = 61_100_840, reps: int = 3) -> dict:
+    """The reference's numpy update rules (updates.py:85-140, via the oracle's
+    restatement) on n fp32 parameters: algorithmic GB/s (worker 16 B, center
+    from sum 12 B, MEASGD 24 B per parameter), best of reps."""
+    from oracle import esgd_oracle as O
+
+    rng = np.random.default_rng(0)
+    w, g, c, s, v = (rng.standard_normal(n, dtype=np.float32) for _ in range(5))
+    out = {}
+    for name, fn, bpp in (("easgd_worker_step", lambda: O.easgd_worker_step(w, g, c, 0.01, 0.1), 16),
+                          ("easgd_center_step_from_sum", lambda: O.easgd_center_step_from_sum(c, s, 1, 0.01, 0.1), 12),
+                          ("measgd_worker_step", lambda: O.measgd_worker_step(w, v, g, c, 0.01, 0.9, 0.1), 24)):
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            t = time.perf_counter() - t0
+            best = t if best is None else min(best, t)
+        out[name] = round(bpp * n / best / 1e9, 2)
+    out["params"] = n
+    out["unit"] = "GB/s (algorithmic bytes)"
+    return out
+
+
+def threaded_round(args, train, workers: int) -> dict:
+    """One round of the reference's threaded engine (trainers/synchronous.py:
+    156-219, restated as oracle.run_sync_threaded): P OS threads, 3 barriers."""
+    from oracle import esgd_oracle as O
+
+    layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK, "alexnet": O.alexnet_layers(1000)}[args.model]
+    wl = WORKLOADS[args.model]
+    b = args.batch or wl["b"]
+    prob = O.NetProblem(*layers, train.samples, train.labels, seed=0, dtype=np.float32)
+    O.run_sync_threaded(prob, workers, 1, b, wl["eta"], wl["rho"], seed=3)  # warm-up
+    t0 = time.perf_counter()
+    O.run_sync_threaded(prob, workers, 1, b, wl["eta"], wl["rho"], seed=3)
+    t = time.perf_counter() - t0
+    return {"value": round(workers * b / t, 2), "unit": "samples/s", "workers": workers,
+            "sample": f"1 round, P={workers} threads, b={b}/worker"}
 
 
 def cpu_baseline(args, spec, train, budget_s: float = 12.0):
     cpu = CpuRound(args, train)
     rounds, elapsed = cpu.sample(budget_s)
-    return {"value": round(rounds * cpu.b / elapsed, 2), "unit": "samples/s", "cores": cpu.cores,
-            "kind": "port", "sample": cpu.describe(rounds)}
+    out = {"value": round(rounds * cpu.b / elapsed, 2), "unit": "samples/s", "cores": cpu.cores,
+           "kind": "port", "sample": cpu.describe(rounds), "host": host_info()}
+    try:
+        out["update_rules"] = update_rules_gbs(spec.parameter_count())
+        out["threaded_engine"] = threaded_round(args, train, 2)
+    except Exception as exc:  # extras only; never fail the bench over them
+        out["extras_error"] = repr(exc)
+    return out
 
 
 def run_reference(args):
     """--impl reference: the reference's CPU algorithm (the oracle port — the
     reference is pure Python/numpy and is not installed on the GPU box) on the
-    host's cores, same metric/config as the native arm. Each step is a bounded
-    sample (>= 1 round, ~1 s) so the whole run stays within a few minutes."""
+    host's cores, on the native arm's config: P = N workers (one per GPU),
+    b per worker, full rounds. Rank 0 alone runs it. Each step is one full
+    round; when K rounds would exceed ~150 s, fewer are timed (stated in
+    the sample) so the run ends within a few minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_1708_02983_b200 import network
 
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     spec = network.MODELS[args.model](seed=0)
     train, _ = make_data(args.model, spec)
-    wl = WORKLOADS[args.model]
-    b = args.batch or wl["b"]
-    cpu = CpuRound(args, train)
-    per_step = min(2.0, 120.0 / max(1, args.steps + args.warmup))
+    cpu = CpuRound(args, train, workers=world)  # includes one warm-up round
+    t_round = None
     tot_r, tot_t = 0, 0.0
-    for i in range(args.steps + args.warmup):
-        r, t = cpu.sample(per_step)
-        if i >= args.warmup:
-            tot_r, tot_t = tot_r + r, tot_t + t
-    value = round(tot_r * cpu.b / tot_t, 2)
+    min_step = 0.25  # small models: several rounds per step so timer noise stays small
+    for i in range(args.steps):
+        r, t = cpu.sample(min_step)
+        tot_r, tot_t = tot_r + r, tot_t + t
+        t_round = tot_t / tot_r
+        if i >= 2 and tot_t + t_round * (args.steps - i - 1) > 150.0:
+            break
+    steps_done = i + 1
+    value = round(tot_r * cpu.P * cpu.b / tot_t, 2)
     out = {"impl": "reference", "metric": METRIC,
-           "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(1000.0 * tot_t / max(1, args.steps), 3),
+           "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1000.0 * tot_t / steps_done, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic", "config": workload_config(args, b, 1),
+           "data": "synthetic", "config": workload_config(args, cpu.b, world),
            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cpu.cores, "kind": "port",
-                            "sample": cpu.describe(tot_r)},
+                            "sample": cpu.describe(tot_r) + f"; {steps_done} of {args.steps} steps timed "
+                            "(1 warm-up round)", "host": host_info()},
            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

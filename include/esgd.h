@@ -74,6 +74,14 @@ int esgd_sync_update_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg,
                              float* C, const float* S, float* S_next, int64_t n, float eta,
                              float etarho, int32_t num_workers, esgd_stream_t stream);
 
+/* Sync-EASGD round update for a run with ONE worker in total (P = 1, one
+ * process): the sum S = tree_sum([W]) (fabric/collectives.py:18-32) is W(t)
+ * itself, so W <- worker_step(W, G, C), C <- center_step_from_sum(C, W(t), 1)
+ * read W, G, C and write W, C (20 B/param; esgd_sync_update_sum_f32 moves 28).
+ * Bitwise equal to the reference round (trainers/synchronous.py:57-64, P=1). */
+int esgd_sync_update_solo_f32(float* W, const float* G, float* C, int64_t n, float eta, float etarho,
+                              esgd_stream_t stream);
+
 /* Multi-GPU round update fused with its collective over NVLink SHARP
  * (NVLS) multicast (replaces ncclAllReduce(S) + esgd_sync_update_sum_f32):
  * this rank's 1/world slice of the center is updated from the NVSwitch-
@@ -210,6 +218,10 @@ typedef struct {
   int64_t ws_floats;
 } esgd_gemm_desc;
 int esgd_gemm_f32(const esgd_gemm_desc* desc, esgd_stream_t stream);
+/* floats of `ws` esgd_gemm_f32 needs for this problem (0: no K split). The
+ * split depends on the per-replica shape only, so results never depend on
+ * `batch` or the workspace; a smaller `ws` fails with ESGD_ERR_UNSUPPORTED. */
+int esgd_gemm_ws_floats(const esgd_gemm_desc* desc, int64_t* floats);
 
 /* Tensor-core GEMM (tcgen05.mma kind::tf32, TMA-fed, accumulator in TMEM)
  * with 3xTF32 error compensation (hi*hi + hi*lo + lo*hi) and per-128-K
@@ -237,6 +249,9 @@ typedef struct {
   int64_t ws_floats;
 } esgd_tc_gemm_desc;
 int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* desc, esgd_stream_t stream);
+/* floats of `ws` esgd_tc_gemm_f32 needs for this problem (0: no K split);
+ * same contract as esgd_gemm_ws_floats.                                    */
+int esgd_tc_gemm_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
 
 /* activation forward/backward, kernels.py:30-70.
  * act_fwd: y = act(z); act_bwd: d = d * act'(z) (in place).                 */

@@ -21,7 +21,11 @@ arm may import this module.
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
+from numpy.lib.stride_tricks import sliding_window_view
 
 # ---------------------------------------------------------------------------
 # rng.py:30-105
@@ -236,16 +240,46 @@ def build_model(input_shape, layers, seed, dtype):
     return buf
 
 
+# Data-movement helpers of the CNN restatement. They are pure copies / fixed-
+# order accumulations, written with strided views and split over the batch
+# across host threads (ESGD_ORACLE_THREADS, default all cores): per element the
+# values and the accumulation order are those of the plain per-tap loops
+# (tests/test_oracle_cnn.py pins them against those loops), only faster, so the
+# CPU baseline is not dominated by slow numpy indexing.
+_POOL = None
+
+
+def _nthreads():
+    return max(1, int(os.environ.get("ESGD_ORACLE_THREADS", os.cpu_count() or 1)))
+
+
+def _par(fn, n, size):
+    """fn(a, b) over batch chunks [a, b) on the thread pool (one chunk when small)."""
+    global _POOL
+    t = min(_nthreads(), n) if size >= (1 << 20) else 1
+    bounds = np.linspace(0, n, t + 1).astype(int)
+    chunks = [(int(bounds[i]), int(bounds[i + 1])) for i in range(t) if bounds[i + 1] > bounds[i]]
+    if len(chunks) == 1:
+        fn(*chunks[0])
+        return
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(_nthreads())
+    list(_POOL.map(lambda c: fn(*c), chunks))
+
+
 def _im2col(x, k, s, p):
     """x (n, c, h, w) -> col (n*oh*ow, c*k*k) with column order (ci, ky, kx)."""
     n, c, h, w = x.shape
     oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
-    xp = np.zeros((n, c, h + 2 * p, w + 2 * p), dtype=x.dtype)
-    xp[:, :, p:p + h, p:p + w] = x
     col = np.empty((n, oh, ow, c, k, k), dtype=x.dtype)
-    for ky in range(k):
-        for kx in range(k):
-            col[:, :, :, :, ky, kx] = xp[:, :, ky:ky + s * oh:s, kx:kx + s * ow:s].transpose(0, 2, 3, 1)
+
+    def part(a, b):
+        xp = np.zeros((b - a, c, h + 2 * p, w + 2 * p), dtype=x.dtype)
+        xp[:, :, p:p + h, p:p + w] = x[a:b]
+        v = sliding_window_view(xp, (k, k), axis=(2, 3))[:, :, ::s, ::s][:, :, :oh, :ow]
+        col[a:b] = v.transpose(0, 2, 3, 1, 4, 5)
+
+    _par(part, n, col.size)
     return col.reshape(n * oh * ow, c * k * k), oh, ow
 
 
@@ -253,11 +287,18 @@ def _col2im(dcol, shape, k, s, p, oh, ow):
     """Adjoint of _im2col; accumulation order per input element is (ky, kx)."""
     n, c, h, w = shape
     d = dcol.reshape(n, oh, ow, c, k, k)
-    dxp = np.zeros((n, c, h + 2 * p, w + 2 * p), dtype=dcol.dtype)
-    for ky in range(k):
-        for kx in range(k):
-            dxp[:, :, ky:ky + s * oh:s, kx:kx + s * ow:s] += d[:, :, :, :, ky, kx].transpose(0, 3, 1, 2)
-    return dxp[:, :, p:p + h, p:p + w]
+    dx = np.empty((n, c, h, w), dtype=dcol.dtype)
+
+    def part(a, b):
+        dT = np.ascontiguousarray(d[a:b].transpose(0, 3, 4, 5, 1, 2))  # (m, c, k, k, oh, ow)
+        dxp = np.zeros((b - a, c, h + 2 * p, w + 2 * p), dtype=dcol.dtype)
+        for ky in range(k):
+            for kx in range(k):
+                dxp[:, :, ky:ky + s * oh:s, kx:kx + s * ow:s] += dT[:, :, ky, kx]
+        dx[a:b] = dxp[:, :, p:p + h, p:p + w]
+
+    _par(part, n, dcol.size)
+    return dx
 
 
 def _maxpool(x, k, s, p):
@@ -265,32 +306,48 @@ def _maxpool(x, k, s, p):
     (ky, kx) scan order, as flat h*W+w of the input plane."""
     n, c, h, w = x.shape
     oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
-    best = np.full((n, c, oh, ow), -np.inf, dtype=x.dtype)
-    arg = np.full((n, c, oh, ow), -1, dtype=np.int64)
-    for ky in range(k):
-        for kx in range(k):
-            iy = np.arange(oh) * s - p + ky
-            ix = np.arange(ow) * s - p + kx
-            vy, vx = (iy >= 0) & (iy < h), (ix >= 0) & (ix < w)
-            cand = np.full((n, c, oh, ow), -np.inf, dtype=x.dtype)
-            sub = x[:, :, np.clip(iy, 0, h - 1)][:, :, :, np.clip(ix, 0, w - 1)]
-            valid = vy[:, None] & vx[None, :]
-            cand[:, :, valid] = sub[:, :, valid]
-            flat = (iy[:, None] * w + ix[None, :])
-            upd = (cand > best) | ((arg < 0) & valid[None, None])
-            best = np.where(upd, cand, best)
-            arg = np.where(upd, np.broadcast_to(flat, arg.shape), arg)
+    best = np.empty((n, c, oh, ow), dtype=x.dtype)
+    arg = np.empty((n, c, oh, ow), dtype=np.int64)
+
+    def part(a, b):
+        m = b - a
+        hp, wp = max(h + 2 * p, (oh - 1) * s + k), max(w + 2 * p, (ow - 1) * s + k)
+        xp = np.full((m, c, hp, wp), -np.inf, dtype=x.dtype)
+        xp[:, :, p:p + h, p:p + w] = x[a:b]
+        bst = np.full((m, c, oh, ow), -np.inf, dtype=x.dtype)
+        ag = np.full((m, c, oh, ow), -1, dtype=np.int64)
+        for ky in range(k):
+            for kx in range(k):
+                iy = np.arange(oh) * s - p + ky
+                ix = np.arange(ow) * s - p + kx
+                valid = ((iy >= 0) & (iy < h))[:, None] & ((ix >= 0) & (ix < w))[None, :]
+                cand = xp[:, :, ky:ky + s * (oh - 1) + 1:s, kx:kx + s * (ow - 1) + 1:s]
+                cand = np.where(valid, cand, -np.inf).astype(x.dtype, copy=False)
+                upd = (cand > bst) | ((ag < 0) & valid)
+                np.copyto(bst, cand, where=upd)
+                np.copyto(ag, np.broadcast_to(iy[:, None] * w + ix[None, :], ag.shape), where=upd)
+        best[a:b], arg[a:b] = bst, ag
+
+    _par(part, n, x.size)
     return best, arg
 
 
 def _maxpool_bwd(dy, arg, shape):
+    """dx[argmax] += dy, outputs visited in (oy, ox) order (the device's
+    gather order)."""
     n, c, h, w = shape
-    dx = np.zeros((n, c, h * w), dtype=dy.dtype)
-    nn, cc = np.meshgrid(np.arange(n), np.arange(c), indexing="ij")
     oh, ow = dy.shape[2:]
-    for oy in range(oh):            # output order (oy, ox): the device's gather order
-        for ox in range(ow):
-            np.add.at(dx, (nn, cc, arg[:, :, oy, ox]), dy[:, :, oy, ox])
+    dx = np.zeros((n, c, h * w), dtype=dy.dtype)
+
+    def part(a, b):
+        sub = dx[a:b]
+        nn, cc = np.meshgrid(np.arange(b - a), np.arange(c), indexing="ij")
+        for oy in range(oh):
+            for ox in range(ow):
+                # one target per (n, c) plane per output: no duplicate indices
+                sub[nn, cc, arg[a:b, :, oy, ox]] += dy[a:b, :, oy, ox]
+
+    _par(part, n, dx.size)
     return dx.reshape(n, c, h, w)
 
 
@@ -545,3 +602,44 @@ def interleaved_apply(center, delta_fns, rng, num_blocks=8):
             order[i], order[j] = order[j], order[i]
         for i in order:
             center[sl] += fns[i](center[sl], sl)
+
+
+# ---------------------------------------------------------------------------
+# trainers/synchronous.py:156-219 (the reference's threaded engine: one OS
+# thread per worker, three barriers per round, thread 0 sums in tree order and
+# steps the center; the worker step uses the pre-update center snapshot)
+
+def run_sync_threaded(problem, workers, iterations, batch_size, eta, rho, seed, groups=1):
+    import threading
+
+    rngs = [worker_rng(seed, w) for w in range(workers)]
+    init = problem.init_weights()
+    W = [init.copy() for _ in range(workers)]
+    grads = [None] * workers
+    shared = {"center": init.copy(), "snap": None, "failure": None}
+    barrier = threading.Barrier(workers)
+
+    def body(w):
+        try:
+            for _ in range(iterations):
+                grads[w] = problem.gradient(W[w], rngs[w], batch_size)
+                barrier.wait()
+                if w == 0:
+                    s = grouped_tree_sum(W, groups)
+                    shared["snap"] = shared["center"]
+                    shared["center"] = easgd_center_step_from_sum(shared["center"], s, workers, eta, rho)
+                barrier.wait()
+                W[w] = easgd_worker_step(W[w], grads[w], shared["snap"], eta, rho)
+                barrier.wait()
+        except Exception as exc:  # surfaced to the caller (synchronous.py:209-210)
+            shared["failure"] = exc
+            barrier.abort()
+
+    threads = [threading.Thread(target=body, args=(w,)) for w in range(workers)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if shared["failure"] is not None:
+        raise shared["failure"]
+    return shared["center"], W

@@ -87,6 +87,7 @@ _SIGS = {
     "esgd_worker_step_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, f32, f32, vp]),
     "esgd_sync_update_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, vp, i64, f32, f32, i32, vp]),
     "esgd_measgd_update_f32": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, f32, vp]),
+    "esgd_sync_update_solo_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
     "esgd_center_incr_f32": (C.c_int, [vp, vp, vp, i64, f32, vp]),
     "esgd_exchange_update_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
     "esgd_sgd_step_f32": (C.c_int, [vp, vp, i64, f32, vp]),
@@ -100,6 +101,8 @@ _SIGS = {
     "esgd_quadratic_grad_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, vp]),
     "esgd_gemm_f32": (C.c_int, [C.POINTER(GemmDesc), vp]),
     "esgd_tc_gemm_f32": (C.c_int, [C.POINTER(TcGemmDesc), vp]),
+    "esgd_gemm_ws_floats": (C.c_int, [C.POINTER(GemmDesc), C.POINTER(i64)]),
+    "esgd_tc_gemm_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_act_fwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),
     "esgd_act_bwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),
     "esgd_softmax_xent_f32": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, i32, i32, i32, vp, vp]),

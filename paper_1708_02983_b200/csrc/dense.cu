@@ -338,25 +338,27 @@ __global__ void __launch_bounds__(256) k_transpose(float* __restrict__ dst, int6
 using namespace esgd;
 #define ESGD_STREAM(s) reinterpret_cast<cudaStream_t>(s)
 
-extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
-  ESGD_REQUIRE(d, ESGD_ERR_INPUT, "gemm: null descriptor");
-  ESGD_REQUIRE(d->m >= 0 && d->n >= 0 && d->k >= 0 && d->batch >= 0, ESGD_ERR_SHAPE,
-               "gemm shape mismatch: m=%d n=%d k=%d batch=%d", d->m, d->n, d->k, d->batch);
-  ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "gemm: unknown activation %d", d->act);
-  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
-  ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
-  ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
+namespace esgd {
+namespace {
+// Tile and K split of one FFMA GEMM. The split depends on the per-replica
+// problem only (never on `batch` or the workspace size): replicas compute
+// bit-identical results whatever the launch groups them with. A NULL
+// workspace means "do not split"; one that is too small is an error.
+struct FfmaPlan {
+  bool small;
+  int splits, kchunk;
+};
+FfmaPlan ffma_plan(const esgd_gemm_desc* d) {
   // tuning knobs (read once): ESGD_FFMA_TILE = 32 / 64 forces the tile,
   // ESGD_FFMA_MAXSPLIT caps the K split
   static const int force_tile = getenv("ESGD_FFMA_TILE") ? atoi(getenv("ESGD_FFMA_TILE")) : 0;
   static const int max_split = getenv("ESGD_FFMA_MAXSPLIT") ? atoi(getenv("ESGD_FFMA_MAXSPLIT")) : 128;
+  FfmaPlan p;
   // 32x32 tiles only for outputs that are <= 32 wide on one side (a 64-wide
   // tile would be mostly padding); measured per LeNet GEMM: conv1 fwd
   // (N = 20) 17.1 -> 12.7 us, conv2 fwd / wgrad 30.9 -> 24.7 / 35.1 -> 23.4 us
-  const bool small = force_tile ? force_tile == 32 : (d->m <= 32 || d->n <= 32);
-  const int TM = small ? 32 : 64, TN = TM;
-  // the K split depends on the per-entry problem only (never on `batch`):
-  // replicas compute bit-identical results whatever the launch groups them with
+  p.small = force_tile ? force_tile == 32 : (d->m <= 32 || d->n <= 32);
+  const int TM = p.small ? 32 : 64, TN = TM;
   const int tiles = ((d->n + TN - 1) / TN) * ((d->m + TM - 1) / TM);
   int splits = 1;
   if (d->ws && tiles < 2 * kNumSMs && d->k >= 4 * BK * 4) {
@@ -366,14 +368,47 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
     splits = want < maxs ? want : maxs;
     if (splits > max_split) splits = max_split;
     if (splits < 1) splits = 1;
-    if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats || (int64_t)d->batch * splits > 65535)
-      splits = 1;
   }
-  const int kchunk = ((d->k + splits - 1) / splits + BK - 1) / BK * BK;
-  if (splits > 1) splits = (d->k + kchunk - 1) / kchunk;
+  p.kchunk = ((d->k + splits - 1) / splits + BK - 1) / BK * BK;
+  p.splits = splits > 1 ? (d->k + p.kchunk - 1) / p.kchunk : 1;
+  return p;
+}
+}  // namespace
+}  // namespace esgd
+
+extern "C" int esgd_gemm_ws_floats(const esgd_gemm_desc* d, int64_t* floats) {
+  using namespace esgd;
+  ESGD_REQUIRE(d && floats, ESGD_ERR_INPUT, "gemm_ws_floats: null argument");
+  *floats = 0;
+  if (d->m <= 0 || d->n <= 0 || d->batch <= 0 || d->k <= 0) return ESGD_OK;
+  esgd_gemm_desc q = *d;
+  if (!q.ws) q.ws = reinterpret_cast<float*>(uintptr_t(256));
+  const FfmaPlan p = ffma_plan(&q);
+  *floats = p.splits > 1 ? (int64_t)p.splits * d->m * d->n * d->batch : 0;
+  return ESGD_OK;
+}
+
+extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
+  ESGD_REQUIRE(d, ESGD_ERR_INPUT, "gemm: null descriptor");
+  ESGD_REQUIRE(d->m >= 0 && d->n >= 0 && d->k >= 0 && d->batch >= 0, ESGD_ERR_SHAPE,
+               "gemm shape mismatch: m=%d n=%d k=%d batch=%d", d->m, d->n, d->k, d->batch);
+  ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "gemm: unknown activation %d", d->act);
+  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
+  ESGD_REQUIRE(d->c && (d->k == 0 || (d->a && d->b)), ESGD_ERR_INPUT, "gemm: null operand");
+  ESGD_REQUIRE(d->batch <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch > 65535");
+  const esgd::FfmaPlan p = esgd::ffma_plan(d);
+  const int splits = p.splits, kchunk = p.kchunk;
+  const int TM = p.small ? 32 : 64, TN = TM;
+  if (splits > 1) {
+    const int64_t need = (int64_t)splits * d->m * d->n * d->batch;
+    ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
+                 "gemm: split-K workspace too small (need %lld floats, have %lld; size it with "
+                 "esgd_gemm_ws_floats)", (long long)need, (long long)d->ws_floats);
+    ESGD_REQUIRE((int64_t)d->batch * splits <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: batch x K split > 65535");
+  }
   dim3 grid((d->n + TN - 1) / TN, (d->m + TM - 1) / TM, d->batch * splits);
   ESGD_REQUIRE(grid.y <= 65535, ESGD_ERR_UNSUPPORTED, "gemm: m too large for the FFMA path");
-  if (small) k_gemm<32, 32><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
+  if (p.small) k_gemm<32, 32><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
   else k_gemm<64, 64><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
   if (splits > 1) {
     dim3 rgrid(stride_grid((int64_t)d->m * d->n, 256, 4), d->batch);

@@ -802,9 +802,64 @@ inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
   return padded(m, BM) * padded(n, pick_bn(m, n, split));
 }
 
+// Launch plan of one GEMM: orientation (C^T = B.A^T when it needs less padded
+// tensor-core work), tile width and K split.
+struct Plan {
+  esgd_tc_gemm_desc d;  // the oriented problem
+  int bn, splits, kbps;
+};
+
+inline Plan make_plan(const esgd_tc_gemm_desc* d0) {
+  Plan p;
+  p.d = *d0;
+  const bool split = d0->precision == 3;
+  // Orientation: C^T = B . A^T is the same GEMM with the operands' roles
+  // swapped; take it when it needs less padded tensor-core work (M is tiled
+  // by 128: a 64- or 192-row M wastes half / a quarter of every MMA). Only
+  // without a per-column bias (the epilogue applies bias along N).
+  if (!d0->bias && padded_cost(d0->n, d0->m, split) < padded_cost(d0->m, d0->n, split)) {
+    esgd_tc_gemm_desc& sw = p.d;
+    sw.m = d0->n; sw.n = d0->m;
+    sw.a = d0->b; sw.lda = d0->ldb; sw.a_sb = d0->b_sb; sw.a_major = d0->b_major;
+    sw.b = d0->a; sw.ldb = d0->lda; sw.b_sb = d0->a_sb; sw.b_major = d0->a_major;
+    sw.c_sm = d0->c_sn; sw.c_sn = d0->c_sm;
+    sw.mask_sm = d0->mask_sn; sw.mask_sn = d0->mask_sm;
+  }
+  const esgd_tc_gemm_desc* d = &p.d;
+  p.bn = pick_bn(d->m, d->n, split);
+  const int nkb = (d->k + BK - 1) / BK;
+  // The K split depends on the per-replica problem only, never on `batch` or
+  // on the workspace size: a replica computes bit-identical results however
+  // many replicas share the launch, so runs are reproducible across GPU
+  // counts. Split when the output tiles cannot fill the 148 SMs (weight
+  // gradients reduce over every pixel of the batch): ~1 wave, >= 2 chunks per
+  // slice (2 waves: conv2.wgrad 0.30 vs 0.28 ms and a ~2% slower round - twice
+  // the partials for k_tc_reduce; 3-4 far worse). A NULL workspace means "do
+  // not split"; a workspace that is too small is an error (esgd_tc_gemm_f32
+  // returns ESGD_ERR_UNSUPPORTED; size it with esgd_tc_gemm_ws_floats).
+  const int tiles_z = ((d->n + p.bn - 1) / p.bn) * ((d->m + BM - 1) / BM);
+  int splits = 1;
+  if (d->ws && tiles_z < kNumSMs && nkb >= 2 * kChunkKB) {
+    splits = (ESGD_SPLIT_WAVES * kNumSMs) / tiles_z;
+    splits = std::min(splits, nkb / (2 * kChunkKB));
+    splits = std::min(splits, 128);
+    if (splits < 1) splits = 1;
+  }
+  int kbps = (nkb + splits - 1) / splits;
+  kbps = (kbps + kChunkKB - 1) / kChunkKB * kChunkKB;
+  p.splits = (nkb + kbps - 1) / kbps;
+  p.kbps = kbps;
+  return p;
+}
+
+inline int64_t ws_need(const Plan& p) {
+  return p.splits > 1 ? (int64_t)p.splits * p.d.m * p.d.n * p.d.batch : 0;
+}
+
 template <int BN, bool SPLIT, bool AMN, bool BMN>
-int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
+int launch(const Plan& p, cudaStream_t st) {
   using C = Cfg<BN, SPLIT>;
+  const esgd_tc_gemm_desc* d = &p.d;
   // per-device attribute; cheap, and legal while a stream is being captured
   cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT, AMN, BMN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -815,26 +870,8 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
   if (rc) return rc;
   rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN, BMN);
   if (rc) return rc;
-  const int nkb = (d->k + BK - 1) / BK;
-  // the K split depends on the per-entry problem only (not on `batch`), so a
-  // replica computes bit-identical results however many replicas share the
-  // launch — runs are reproducible across GPU counts
-  const int tiles_z = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM);
-  const int tiles = tiles_z * d->batch;
-  // split K when the output tiles cannot fill the 148 SMs (weight gradients
-  // reduce over every pixel of the batch): ~1 wave, >= 2 chunks per slice (2 waves: conv2.wgrad
-  // 0.30 vs 0.28 ms and a ~2% slower round - twice the partials for k_tc_reduce; 3-4 far worse)
-  int splits = 1;
-  if (d->ws && tiles_z < kNumSMs && nkb >= 2 * kChunkKB) {
-    splits = (ESGD_SPLIT_WAVES * kNumSMs) / tiles_z;
-    splits = std::min(splits, nkb / (2 * kChunkKB));
-    splits = std::min(splits, 128);
-    if ((int64_t)splits * d->m * d->n * d->batch > d->ws_floats) splits = 1;  // never batch-dependent
-    if (splits < 1) splits = 1;
-  }
-  int kbps = (nkb + splits - 1) / splits;
-  kbps = (kbps + kChunkKB - 1) / kChunkKB * kChunkKB;
-  splits = (nkb + kbps - 1) / kbps;
+  const int splits = p.splits, kbps = p.kbps;
+  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
   // output: TMA store when one C stride is unit and the other 16-B aligned
   int out_mode = 0;
   CUtensorMap mc;
@@ -875,22 +912,40 @@ int launch(const esgd_tc_gemm_desc* d, cudaStream_t st) {
 }
 
 template <int BN, bool SPLIT>
-int launch_major(const esgd_tc_gemm_desc* d, cudaStream_t st) {
-  if (d->a_major) return d->b_major ? launch<BN, SPLIT, true, true>(d, st) : launch<BN, SPLIT, true, false>(d, st);
-  return d->b_major ? launch<BN, SPLIT, false, true>(d, st) : launch<BN, SPLIT, false, false>(d, st);
+int launch_major(const Plan& p, cudaStream_t st) {
+  const esgd_tc_gemm_desc* d = &p.d;
+  if (d->a_major) return d->b_major ? launch<BN, SPLIT, true, true>(p, st) : launch<BN, SPLIT, true, false>(p, st);
+  return d->b_major ? launch<BN, SPLIT, false, true>(p, st) : launch<BN, SPLIT, false, false>(p, st);
 }
 
-}  // namespace tc
-}  // namespace esgd
-
-extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream) {
-  using namespace esgd;
+int validate(const esgd_tc_gemm_desc* d) {
   ESGD_REQUIRE(d, ESGD_ERR_INPUT, "tc_gemm: null descriptor");
   ESGD_REQUIRE(d->m >= 0 && d->n >= 0 && d->k >= 0 && d->batch >= 0, ESGD_ERR_SHAPE,
                "tc_gemm shape mismatch: m=%d n=%d k=%d", d->m, d->n, d->k);
   ESGD_REQUIRE(d->precision == 1 || d->precision == 3, ESGD_ERR_INPUT,
                "tc_gemm: precision must be 1 (tf32) or 3 (3xtf32)");
   ESGD_REQUIRE(d->act >= 0 && d->act <= 3, ESGD_ERR_INPUT, "tc_gemm: unknown activation");
+  return ESGD_OK;
+}
+
+}  // namespace tc
+}  // namespace esgd
+
+extern "C" int esgd_tc_gemm_ws_floats(const esgd_tc_gemm_desc* d, int64_t* floats) {
+  using namespace esgd;
+  ESGD_REQUIRE(floats, ESGD_ERR_INPUT, "tc_gemm_ws_floats: null output");
+  *floats = 0;
+  if (int rc = tc::validate(d)) return rc;
+  if (d->m == 0 || d->n == 0 || d->batch == 0 || d->k == 0) return ESGD_OK;
+  esgd_tc_gemm_desc q = *d;
+  if (!q.ws) q.ws = reinterpret_cast<float*>(uintptr_t(256));  // ask: how much would it use
+  *floats = tc::ws_need(tc::make_plan(&q));
+  return ESGD_OK;
+}
+
+extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream) {
+  using namespace esgd;
+  if (int rc = tc::validate(d)) return rc;
   if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
   ESGD_REQUIRE(d->k >= 1 && d->a && d->b && d->c, ESGD_ERR_INPUT, "tc_gemm: null operand");
   ESGD_REQUIRE(d->lda >= (d->a_major ? d->m : d->k) && d->ldb >= (d->b_major ? d->n : d->k) &&
@@ -903,24 +958,14 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
                ESGD_ERR_UNSUPPORTED, "tc_gemm: too many tiles");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool split = d->precision == 3;
-  // Orientation: C^T = B . A^T is the same GEMM with the operands' roles
-  // swapped; take it when it needs less padded tensor-core work (M is tiled
-  // by 128: a 64- or 192-row M wastes half / a quarter of every MMA). Only
-  // without a per-column bias (the epilogue applies bias along N).
-  esgd_tc_gemm_desc sw = *d;
-  const esgd_tc_gemm_desc* use = d;
-  if (!d->bias && tc::padded_cost(d->n, d->m, split) < tc::padded_cost(d->m, d->n, split)) {
-    sw.m = d->n; sw.n = d->m;
-    sw.a = d->b; sw.lda = d->ldb; sw.a_sb = d->b_sb; sw.a_major = d->b_major;
-    sw.b = d->a; sw.ldb = d->lda; sw.b_sb = d->a_sb; sw.b_major = d->a_major;
-    sw.c_sm = d->c_sn; sw.c_sn = d->c_sm;
-    sw.mask_sm = d->mask_sn; sw.mask_sn = d->mask_sm;
-    use = &sw;
-  }
-  const int bn = tc::pick_bn(use->m, use->n, split);
-  if (bn == 64) return split ? tc::launch_major<64, true>(use, st) : tc::launch_major<64, false>(use, st);
-  if (bn == 192) return tc::launch_major<192, true>(use, st);
-  return split ? tc::launch_major<128, true>(use, st) : tc::launch_major<128, false>(use, st);
+  const tc::Plan p = tc::make_plan(d);
+  const int64_t need = tc::ws_need(p);
+  ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
+               "tc_gemm: split-K workspace too small (need %lld floats, have %lld; size it with "
+               "esgd_tc_gemm_ws_floats)", (long long)need, (long long)d->ws_floats);
+  if (p.bn == 64) return split ? tc::launch_major<64, true>(p, st) : tc::launch_major<64, false>(p, st);
+  if (p.bn == 192) return tc::launch_major<192, true>(p, st);
+  return split ? tc::launch_major<128, true>(p, st) : tc::launch_major<128, false>(p, st);
 }
 
 #ifdef ESGD_TRACE

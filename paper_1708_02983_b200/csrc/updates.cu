@@ -14,9 +14,10 @@ namespace esgd {
 namespace {
 
 // ---- worker / center rules ------------------------------------------------
+// (outputs are not __restrict__: the in-place callers pass wo == w)
 
 template <int V>
-__global__ void __launch_bounds__(256) k_worker_step(float* __restrict__ wo, const float* w,
+__global__ void __launch_bounds__(256) k_worker_step(float* wo, const float* w,
                                                      const float* __restrict__ g,
                                                      const float* __restrict__ c, int64_t n,
                                                      float eta, float er) {
@@ -398,6 +399,46 @@ __global__ void __launch_bounds__(256) k_sync_update_sum4(float* W, int64_t ldw,
     C[j] = center_rule(c, s, p, er);
     S_next[j] = binomial_sum<MAXP>(v, nrep);
   }
+}
+
+// One worker in total (P = 1): the round's sum S = tree_sum([W]) is W(t)
+// itself, so the update reads W, G, C and writes W, C — 20 B/param instead
+// of the 28 of k_sync_update_sum4 (no S read, no S_next write). Bitwise the
+// reference's round: center_rule(c, w(t), 1, er) with the pre-update w.
+__global__ void __launch_bounds__(256) k_sync_update_solo4(float* W, const float* __restrict__ G, float* C,
+                                                           int64_t n, float eta, float er) {
+  const int64_t nv = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 c = ld4rw(C + 4 * i), w = ld4rw(W + 4 * i), g = ld4(G + 4 * i);
+    float4 o, q;
+    o.x = worker_rule(w.x, g.x, c.x, eta, er);
+    o.y = worker_rule(w.y, g.y, c.y, eta, er);
+    o.z = worker_rule(w.z, g.z, c.z, eta, er);
+    o.w = worker_rule(w.w, g.w, c.w, eta, er);
+    q.x = center_rule(c.x, w.x, 1.f, er);
+    q.y = center_rule(c.y, w.y, 1.f, er);
+    q.z = center_rule(c.z, w.z, 1.f, er);
+    q.w = center_rule(c.w, w.w, 1.f, er);
+    st4(W + 4 * i, o);
+    st4(C + 4 * i, q);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t j = (n & ~int64_t(3)) + threadIdx.x;
+    const float c = C[j], w = W[j];
+    W[j] = worker_rule(w, G[j], c, eta, er);
+    C[j] = center_rule(c, w, 1.f, er);
+  }
+}
+
+extern "C" int esgd_sync_update_solo_f32(float* W, const float* G, float* C, int64_t n, float eta,
+                                         float etarho, esgd_stream_t stream) {
+  ESGD_REQUIRE(n >= 0, ESGD_ERR_SHAPE, "sync_update_solo: negative length");
+  if (n == 0) return ESGD_OK;
+  ESGD_REQUIRE(W && G && C, ESGD_ERR_INPUT, "sync_update_solo: null buffer");
+  ESGD_REQUIRE(vec_ok({W, G, C}), ESGD_ERR_UNSUPPORTED, "sync_update_solo: buffers must be 16-B aligned");
+  k_sync_update_solo4<<<stride_grid(n / 4 + 1, 256), 256, 0, ESGD_STREAM(stream)>>>(W, G, C, n, eta, etarho);
+  return check_launch("esgd_sync_update_solo_f32");
 }
 
 extern "C" int esgd_center_step_from_sum_f32(float* c_out, const float* c, const float* s,

@@ -156,14 +156,27 @@ def load_state(path, engine) -> int:
     buf = io.BytesIO(raw)
     if buf.read(4) != STATE_MAGIC:
         raise DataFormatError("bad state magic", offset=0)
+    if len(raw) < 8:
+        raise DataFormatError("truncated state header", offset=len(raw))
     (hl,) = struct.unpack("<I", buf.read(4))
-    head = json.loads(buf.read(hl))
+    if 8 + hl > len(raw):
+        raise DataFormatError(f"state header of {hl} bytes runs past the end of the file", offset=8)
+    try:
+        head = json.loads(buf.read(hl))
+    except ValueError as exc:
+        raise DataFormatError(f"unreadable state header: {exc}", offset=8) from exc
     n, P = engine.n, engine.P
     if head["n"] != n or head["workers"] != P or head["method"] != engine.cfg.method:
         raise InputError(f"state {head['method']} P={head['workers']} n={head['n']} does not match the engine")
     fp = getattr(engine.problem, "fingerprint", lambda: "")()
     if head.get("fingerprint") and fp and head["fingerprint"] != fp:
         raise InputError("state was written for a different problem (fingerprint mismatch)")
+    # check every payload length before anything is copied into the engine
+    expect = 8 + hl + 4 * n + 4 * n * engine.nrep + 16 * int(head.get("rng_rows", 0))
+    if len(raw) != expect:
+        raise DataFormatError(f"state payload is {len(raw)} bytes, expected {expect} "
+                              f"(header + center + {engine.nrep} workers + RNG rows)",
+                              offset=min(len(raw), expect))
     C = np.frombuffer(buf.read(4 * n), dtype="<f4")
     W = np.frombuffer(buf.read(4 * n * engine.nrep), dtype="<f4").reshape(engine.nrep, n)
     rng = np.frombuffer(buf.read(16 * head["rng_rows"]), dtype="<u8").reshape(-1, 2)

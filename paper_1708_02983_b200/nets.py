@@ -48,6 +48,30 @@ import os
 TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 28)))
 
 
+class _FakeRows:
+    """Stand-in for the (nrep, ldw) weight / gradient tensors during the
+    launch-free workspace-planning pass (only pointers and strides are read)."""
+
+    def __init__(self, ldw: int):
+        self.ldw = ldw
+
+    def data_ptr(self) -> int:
+        return 1 << 20
+
+    def stride(self, dim: int) -> int:
+        return self.ldw
+
+
+class _NullLib:
+    """libesgd stand-in for the planning pass: every launcher is a no-op."""
+
+    def __getattr__(self, name):
+        return lambda *args: 0
+
+
+_NULL_LIB = _NullLib()
+
+
 @dataclass
 class _Layer:
     kind: str                  # conv | pool | dense
@@ -150,9 +174,10 @@ class DeviceNet:
         self.dcol = self._t(max((L.k * L.np4 for L in self.layers if L.kind == "conv"), default=4))
         self.scratch = torch.zeros(256 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
-        # split-K partials of the FFMA GEMM (weight gradients reduce over b*OH*OW)
-        self.gemm_ws = torch.zeros(1 << 22, dtype=torch.float32, device=self.device)
-        self.tc_ws = torch.zeros(1 << 23, dtype=torch.float32, device=self.device)
+        # split-K partials of the GEMMs (weight gradients reduce over b*OH*OW),
+        # sized below from the plan's own GEMMs (the libraries error out rather
+        # than change the split when a workspace is short)
+        self.gemm_ws = self.tc_ws = None
         # conv weights whose row (K) is not a multiple of 4 floats get a padded
         # copy each round so the forward GEMM can take them through TMA
         self.wpad = [self._t(L.cout * L.kp) if (L.kind == "conv" and L.k % 4) else None for L in self.layers]
@@ -168,6 +193,23 @@ class DeviceNet:
             self.dT.append(self._t(L.cout * round_up(b, 4)) if big else None)
         self.tc_calls = self.ffma_calls = 0
         self.record = None  # list to capture (kind, descriptor, flops) of each GEMM launch
+        self._dry = None
+        self._size_workspaces()
+
+    def _size_workspaces(self) -> None:
+        """Walk one gradient pass without launching anything and ask each
+        GEMM how much split-K workspace it uses (esgd_*gemm_ws_floats)."""
+        self._dry = {"tc": 0, "ffma": 0}
+        fake = _FakeRows(self.ldw)
+        try:
+            self.gradient(fake, fake, 0)
+        finally:
+            need, self._dry = self._dry, None
+        self.tc_ws = torch.zeros(max(4, need["tc"]), dtype=torch.float32, device=self.device)
+        self.gemm_ws = torch.zeros(max(4, need["ffma"]), dtype=torch.float32, device=self.device)
+
+    def _L(self):
+        return _NULL_LIB if self._dry is not None else _lib.load()
 
     def _out_desc(self, i: int) -> Tensor4:
         L = self.layers[i]
@@ -193,17 +235,30 @@ class DeviceNet:
                     tc = (a_major, b_major, lda, ldb)
         if tc is not None:
             a_major, b_major, lda, ldb = tc
+            ws = self.tc_ws
             d = TcGemmDesc(m, n, k, nb, a, lda, a_sb, bm, ldb, b_sb, c, c_sm, c_sn, c_sb,
                            bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, act, 0, self.precision,
-                           a_major, b_major, self.tc_ws.data_ptr(), self.tc_ws.numel())
+                           a_major, b_major, ws.data_ptr() if ws is not None else None,
+                           ws.numel() if ws is not None else 0)
+            if self._dry is not None:
+                need = C.c_int64(0)
+                _lib.check(_lib.load().esgd_tc_gemm_ws_floats(C.byref(d), C.byref(need)), "tc_gemm_ws")
+                self._dry["tc"] = max(self._dry["tc"], need.value)
+                return
             _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream), "tc_gemm")
             self.tc_calls += 1
             if self.record is not None:
                 self.record.append(("tc", d, 2.0 * m * n * k * nb))
         else:
+            ws = self.gemm_ws
             d = GemmDesc(m, n, k, nb, a, a_sm, a_sk, a_sb, bm, b_sk, b_sn, b_sb, c, c_sm, c_sn, c_sb,
                          bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, pre, act, 0,
-                         self.gemm_ws.data_ptr(), self.gemm_ws.numel())
+                         ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0)
+            if self._dry is not None:
+                need = C.c_int64(0)
+                _lib.check(_lib.load().esgd_gemm_ws_floats(C.byref(d), C.byref(need)), "gemm_ws")
+                self._dry["ffma"] = max(self._dry["ffma"], need.value)
+                return
             _lib.check(_lib.load().esgd_gemm_f32(C.byref(d), stream), "gemm")
             self.ffma_calls += 1
             if self.record is not None:
@@ -213,7 +268,7 @@ class DeviceNet:
     def forward(self, W: torch.Tensor, stream: int, x: torch.Tensor | None = None) -> torch.Tensor:
         """Forward of all replicas on self.x (or ``x``, same shape); returns
         the logits tensor (nrep, b*classes pitch)."""
-        lib = _lib.load()
+        lib = self._L()
         b, nb = self.b, self.nrep
         wp, ldw = W.data_ptr(), W.stride(0)
         xin = self.x if x is None else x
@@ -277,14 +332,14 @@ class DeviceNet:
 
     def _act_bwd(self, d: torch.Tensor, z_ptr: int, z_sb: int, n_el: int, act: int, stream: int) -> None:
         # d[r] *= act'(z[r]) for each replica (relu'(a) == relu'(z) for a = relu(z))
-        lib = _lib.load()
+        lib = self._L()
         for r in range(self.nrep):
             _lib.check(lib.esgd_act_bwd_f32(d.data_ptr() + 4 * r * d.stride(0), z_ptr + 4 * r * z_sb,
                                             n_el, act, stream), "act_bwd")
 
     def gradient(self, G: torch.Tensor, W: torch.Tensor, stream: int) -> None:
         """G[r] = d(mean CE)/dW[r] on the sampled batch in self.x/self.y."""
-        lib = _lib.load()
+        lib = self._L()
         b, nb = self.b, self.nrep
         wp, ldw = W.data_ptr(), W.stride(0)
         gp, ldg = G.data_ptr(), G.stride(0)

@@ -190,3 +190,16 @@ class HostFedRun:
 
     def step(self) -> float:
         return self.feed.step()
+
+    def close(self) -> None:
+        """Release the feed's graphs and the engine's communicator."""
+        for name in ("graphs", "graph"):
+            if hasattr(self.feed, name):
+                setattr(self.feed, name, None if name == "graph" else [None, None])
+        self.engine.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -38,7 +38,7 @@ from ..fabric.collectives import CabiComm, allreduce_sum_, local_workers, replic
 from ..fabric.nvls import NvlsRound, nvls_fused_single_kernel, nvls_wanted
 from ..fabric.engine import CATEGORIES
 from ..rng import stream_seed
-from ..updates import sync_update_, sync_update_sum_
+from ..updates import sync_update_, sync_update_solo_, sync_update_sum_
 from .common import Recorder
 from .config import TrainerConfig
 from .records import RunRecord
@@ -83,7 +83,10 @@ class SyncEngine:
         # replica sum (esgd_sync_update_sum_f32), so S holds sum_r W_r at the
         # start of every round and the round only allreduces it
         self.fused_sum = self.groups == 1 and self.nrep <= 8
-        if self.fused_sum:
+        # one worker in total: the sum is W(t) itself; the update reads W, G, C
+        # and writes W, C (esgd_sync_update_solo_f32, 20 instead of 28 B/param)
+        self.solo = self.P == 1 and self.world == 1
+        if self.fused_sum and not self.solo:
             replica_sum_(self.S, self.W, self.n)
         # multi-GPU: the round's collective + update as ONE kernel over NVLink
         # SHARP multicast (fabric/nvls.py, csrc/nvls.cu) when the fabric has it;
@@ -127,6 +130,8 @@ class SyncEngine:
 
     # ---- one round ------------------------------------------------------------
     def _sum(self, stream) -> None:
+        if self.solo:
+            return
         if self.nvls is not None:
             if not self.nvls_single:  # center slice over NVLS, overlapped with the backward
                 self.nvls.center(self.parity, self.P, self.cfg.hyper, stream)
@@ -158,6 +163,8 @@ class SyncEngine:
                 self.nvls.update(self.W, self.G, self.parity, self.P, self.cfg.hyper, stream)
             else:
                 self.nvls.workers(self.W, self.G, self.parity, self.cfg.hyper, stream)
+        elif self.solo:
+            sync_update_solo_(self.W, self.G, self.C, self.n, self.cfg.hyper, stream)
         elif self.fused_sum:
             sync_update_sum_(self.W, self.G, self.C, self.S, self.S, self.n, self.P, self.cfg.hyper, stream)
         else:
@@ -204,10 +211,19 @@ class SyncEngine:
             self.graphs = [g, g]
         self.graph = g
 
+    def close(self) -> None:
+        """Release the captured rounds and the C-ABI communicator (if any).
+        Idempotent; the engine cannot step afterwards."""
+        if self.cabi is not None:
+            self.graph, self.graphs = None, [None, None]  # graphs hold work on the communicator
+            torch.cuda.synchronize(self.device)
+            self.cabi.close()
+            self.cabi = None
+
     def after_external_write(self) -> None:
         """W / C were overwritten outside the round (resume): re-form the local
         replica sum the fused update path keeps in S."""
-        if self.fused_sum:
+        if self.fused_sum and not self.solo:
             replica_sum_(self.S, self.W, self.n)
         torch.cuda.synchronize()
 
@@ -291,6 +307,13 @@ def _max_over_ranks(x: float, device) -> float:
 
 def run_synchronous(cfg: TrainerConfig, problem, cm=None, **engine_kw) -> RunRecord:
     eng = SyncEngine(cfg, problem, **engine_kw)
+    try:
+        return _run_rounds(eng, cfg, problem)
+    finally:
+        eng.close()
+
+
+def _run_rounds(eng, cfg: TrainerConfig, problem) -> RunRecord:
     rec = Recorder(problem, cfg.eval_every, cfg.iterations)
     elapsed = 0.0
     t0 = torch.cuda.Event(enable_timing=True)

@@ -165,3 +165,13 @@ def sync_update_(W: torch.Tensor, G: torch.Tensor, C: torch.Tensor, S: torch.Ten
     _lib.call("esgd_sync_update_f32", ptr(W), W.stride(0), ptr(G), G.stride(0), W.shape[0],
               ptr(C), ptr(S), n, hyper.eta32, hyper.etarho32, int(num_workers),
               stream_ptr(stream))
+
+
+def sync_update_solo_(W: torch.Tensor, G: torch.Tensor, C: torch.Tensor, n: int, hyper: HyperParams,
+                      stream=None) -> None:
+    """Round update of a one-worker run (P = 1): S = W(t), so the fused
+    update reads W, G, C and writes W, C only (esgd_sync_update_solo_f32)."""
+    if W.dim() != 2 or W.shape[0] != 1 or G.shape != W.shape:
+        raise ShapeError("sync_update_solo_: W and G must be (1, ld)")
+    _lib.call("esgd_sync_update_solo_f32", ptr(W), ptr(G), ptr(C), n, hyper.eta32, hyper.etarho32,
+              stream_ptr(stream))

@@ -77,3 +77,39 @@ def test_efw1_errors(tmp_path, g):
 
     with pytest.raises(InputError):
         formats.save_weights(p, network.lenet(), np.zeros(10))
+
+
+def test_load_state_rejects_truncated_payload(tmp_path):
+    """ESR1 payload lengths are checked before anything is copied into the
+    engine (truncated / mismatched files -> DataFormatError with an offset)."""
+    import json
+    import struct
+    from types import SimpleNamespace
+
+    import torch
+
+    from paper_1708_02983_b200 import formats
+    from paper_1708_02983_b200.errors import DataFormatError
+
+    n, nrep = 10, 2
+    head = json.dumps({"method": "sync-easgd3", "workers": nrep, "n": n, "rounds_done": 3,
+                       "fingerprint": "", "rng_rows": nrep}).encode()
+    body = formats.STATE_MAGIC + struct.pack("<I", len(head)) + head
+    payload = np.zeros(4 * n + 4 * n * nrep + 16 * nrep, dtype=np.uint8).tobytes()
+    C0 = torch.full((n,), 7.0)
+    eng = SimpleNamespace(n=n, P=nrep, nrep=nrep, cfg=SimpleNamespace(method="sync-easgd3"),
+                          problem=SimpleNamespace(), C=C0, W=torch.zeros(nrep, n))
+    for cut in (1, 17, len(payload) // 2):
+        p = tmp_path / f"s{cut}.esr1"
+        p.write_bytes(body + payload[:-cut])
+        with pytest.raises(DataFormatError):
+            formats.load_state(p, eng)
+    p = tmp_path / "long.esr1"
+    p.write_bytes(body + payload + b"\0")
+    with pytest.raises(DataFormatError):
+        formats.load_state(p, eng)
+    p = tmp_path / "head.esr1"
+    p.write_bytes(formats.STATE_MAGIC + struct.pack("<I", 1000) + head)
+    with pytest.raises(DataFormatError):
+        formats.load_state(p, eng)
+    assert torch.all(C0 == 7.0)  # nothing was copied
