@@ -569,16 +569,24 @@ class QuadProblem:
 # ---------------------------------------------------------------------------
 # trainers/synchronous.py:57-64, 75-153 (arithmetic only; no pricing)
 
-def run_sync(problem, workers, iterations, batch_size, eta, rho, seed, groups=1):
-    rngs = [worker_rng(seed, w) for w in range(workers)]
-    init = problem.init_weights()
-    W = [init.copy() for _ in range(workers)]
-    C = init.copy()
-    for _ in range(iterations):
+def run_sync(problem, workers, iterations, batch_size, eta, rho, seed, groups=1, on_round=None,
+             state=None):
+    """state = (C, W, t0) starts from a given round-t0 state (the workers'
+    RNG counters at t0*batch_size); on_round(t, C, W) sees every state."""
+    if state is None:
+        init = problem.init_weights()
+        W = [init.copy() for _ in range(workers)]
+        C, t0 = init.copy(), 0
+    else:
+        C, W, t0 = state[0].copy(), [w.copy() for w in state[1]], state[2]
+    rngs = [CounterRng(stream_seed(seed, w), t0 * batch_size) for w in range(workers)]
+    for t in range(t0, t0 + iterations):
         grads = [problem.gradient(W[i], rngs[i], batch_size) for i in range(workers)]
         s = grouped_tree_sum(W, groups)
         W = [easgd_worker_step(w, g, C, eta, rho) for w, g in zip(W, grads)]
         C = easgd_center_step_from_sum(C, s, workers, eta, rho)
+        if on_round is not None:
+            on_round(t + 1, C, W)
     return C, W
 
 

@@ -122,10 +122,30 @@ def load_weights(path) -> tuple[tuple[int, ...], np.ndarray]:
 
 # ---- run state (resume) ------------------------------------------------------
 
+def write_state(path, method: str, center, workers, rng_rows, rounds_done: int, fingerprint: str = "") -> None:
+    """ESR1 from host arrays: json header (method, P, n, rounds_done,
+    fingerprint, rng_rows) + the center (n), the worker replicas (P x n) and
+    the workers' RNG (seed, counter) rows, raw little-endian. The format
+    save_state writes; also how a state computed elsewhere (e.g. a CPU run of
+    the reference algorithm) is handed to a device engine (load_state)."""
+    C = np.ascontiguousarray(center, dtype="<f4").reshape(-1)
+    W = np.ascontiguousarray(workers, dtype="<f4").reshape(-1, C.size)
+    rng = np.ascontiguousarray(rng_rows, dtype="<u8").reshape(-1, 2)
+    head = {"method": method, "workers": int(W.shape[0]), "n": int(C.size), "rounds_done": int(rounds_done),
+            "fingerprint": fingerprint, "rng_rows": int(rng.shape[0])}
+    hb = json.dumps(head).encode()
+    with open(path, "wb") as fh:
+        fh.write(STATE_MAGIC)
+        fh.write(struct.pack("<I", len(hb)))
+        fh.write(hb)
+        fh.write(C.tobytes())
+        fh.write(W.tobytes())
+        fh.write(rng.tobytes())
+
+
 def save_state(path, engine, rounds_done: int) -> None:
-    """ESR1: json header (method, P, n, rounds_done, fingerprint) + the
-    engine's center, every local worker replica and the workers' RNG
-    (seed, counter) pairs, raw little-endian. Single-process engines."""
+    """ESR1 of a single-process engine: its center, every local worker
+    replica and the workers' RNG (seed, counter) pairs (write_state)."""
     import torch
 
     if getattr(engine, "world", 1) != 1:
@@ -133,17 +153,10 @@ def save_state(path, engine, rounds_done: int) -> None:
     n = engine.n
     rng = engine.plan.rng.state.detach().cpu().numpy().view("<u8") if hasattr(engine.plan, "rng") else \
         np.zeros((engine.nrep, 2), dtype="<u8")
-    head = {"method": engine.cfg.method, "workers": engine.P, "n": n, "rounds_done": int(rounds_done),
-            "fingerprint": getattr(engine.problem, "fingerprint", lambda: "")(), "rng_rows": int(rng.shape[0])}
-    hb = json.dumps(head).encode()
     torch.cuda.synchronize()
-    with open(path, "wb") as fh:
-        fh.write(STATE_MAGIC)
-        fh.write(struct.pack("<I", len(hb)))
-        fh.write(hb)
-        fh.write(engine.C[:n].detach().cpu().numpy().astype("<f4").tobytes())
-        fh.write(engine.W[:, :n].detach().cpu().numpy().astype("<f4").tobytes())
-        fh.write(rng.tobytes())
+    write_state(path, engine.cfg.method, engine.C[:n].detach().cpu().numpy(),
+                engine.W[:, :n].detach().cpu().numpy(), rng, rounds_done,
+                getattr(engine.problem, "fingerprint", lambda: "")())
 
 
 def load_state(path, engine) -> int:

@@ -92,10 +92,9 @@ def test_quadratic_converges():
 @pytest.mark.parametrize("tc", [True, False])
 def test_sync_cnn_multi_replica_vs_oracle(model, tc, monkeypatch):
     """P workers as batched replicas of one DeviceNet (every CNN kernel runs
-    with batch = P) against the oracle's sequential workers. Three rounds of a
-    randomly-initialised CNN on random data amplify the ~3e-6 per-gradient
-    difference of the tensor-core path, hence 1e-4 here (one-gradient parity
-    is held to 1e-5 in test_gpu_network.py)."""
+    with batch = P) against the oracle's sequential workers, three rounds, at
+    the north-star 1e-5 (measured on the B200: center 3e-9 / 7e-9, workers
+    2e-8 / 3e-8 for LeNet / CIFAR-quick; the fp32 oracle is 4e-8 from fp64)."""
     from paper_1708_02983_b200 import network, nets
 
     if tc:
@@ -109,9 +108,9 @@ def test_sync_cnn_multi_replica_vs_oracle(model, tc, monkeypatch):
     rec = run_trainer(make_config("sync-easgd3", workers=3, iterations=3, batch_size=8, hyper=HY, seed=2), prob)
     oprob = O.NetProblem(*layers, X, Y, seed=1, dtype=np.float32)
     C, W = O.run_sync(oprob, 3, 3, 8, 0.05, 0.25, seed=2)
-    assert rel_err(rec.final_weights, C) < 1e-4
+    assert rel_err(rec.final_weights, C) < 1e-5
     for w_dev, w_ref in zip(rec.final_worker_weights, W):
-        assert rel_err(w_dev, w_ref) < 1e-4
+        assert rel_err(w_dev, w_ref) < 1e-5
 
 
 @pytest.mark.parametrize("model", ["mlp", "lenet"])
