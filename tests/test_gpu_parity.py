@@ -55,11 +55,91 @@ def _configs0():
     return spec, tr.samples, tr.labels
 
 
+def _strided(buf, rows, cols, s_row, s_col, off=0):
+    return torch.as_strided(buf, (rows, cols), (s_row, s_col), off)
+
+
+def _span(rows, cols, s_row, s_col):
+    return (rows - 1) * s_row + (cols - 1) * s_col + 1
+
+
+def test_alexnet_b128_gemm_launches_vs_fp64():
+    """Every tcgen05 GEMM launch of bench.py's AlexNet round (nrep=1, b=128,
+    production routing: the same shapes, majors, pitches, bias/mask/act
+    epilogues, hence the same tile width, split-K count and orientation)
+    re-run on random operands against an fp64 product: <= 1e-5 relative."""
+    import ctypes as C
+
+    from paper_1708_02983_b200 import _lib
+    from paper_1708_02983_b200.device import stream_ptr
+    from paper_1708_02983_b200.nets import DeviceNet
+
+    spec = network.alexnet(num_classes=1000)
+    net = DeviceNet(spec, 128, 1, torch.device("cuda"))
+    W = torch.randn((1, net.ldw), device="cuda") * 0.01
+    G = torch.zeros_like(W)
+    net.x.normal_()
+    net.y.random_(0, 1000)
+    net.record = []
+    net.gradient(G, W, stream_ptr())
+    torch.cuda.synchronize()
+    recs, net.record = net.record, None
+    tcs = [d for kind, d, _ in recs if kind == "tc"]
+    assert len(tcs) >= 10, "AlexNet's contractions should run on tcgen05 at b=128"
+    lib = _lib.load()
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    worst = 0.0
+    for d in tcs:
+        m, n, k = d.m, d.n, d.k
+        assert d.batch == 1
+        a_rows, a_cols = (m, k)
+        sa = (d.lda, 1) if d.a_major == 0 else (1, d.lda)
+        sb = (d.ldb, 1) if d.b_major == 0 else (1, d.ldb)
+        Abuf = torch.randn(_span(m, k, *sa) + 4, device="cuda", generator=gen)
+        Bbuf = torch.randn(_span(n, k, *sb) + 4, device="cuda", generator=gen)
+        Cbuf = torch.zeros(_span(m, n, d.c_sm, d.c_sn) + 4, device="cuda")
+        e = _lib.TcGemmDesc.from_buffer_copy(d)
+        e.a, e.b, e.c = Abuf.data_ptr(), Bbuf.data_ptr(), Cbuf.data_ptr()
+        bias = mask = None
+        if d.bias:
+            bias = torch.randn(n, device="cuda", generator=gen)
+            e.bias = bias.data_ptr()
+        if d.mask:
+            mask = torch.randn(_span(m, n, d.mask_sm, d.mask_sn) + 4, device="cuda", generator=gen)
+            e.mask = mask.data_ptr()
+        need = C.c_int64(0)
+        _lib.check(lib.esgd_tc_gemm_ws_floats(C.byref(e), C.byref(need)))
+        ws = torch.zeros(max(4, need.value), device="cuda")
+        e.ws, e.ws_floats = ws.data_ptr(), ws.numel()
+        _lib.check(lib.esgd_tc_gemm_f32(C.byref(e), stream_ptr()))
+        torch.cuda.synchronize()
+        A = _strided(Abuf, m, k, *sa).double()
+        B = _strided(Bbuf, n, k, *sb).double()
+        ref = A @ B.T
+        if bias is not None:
+            ref = ref + bias.double()
+        if d.act == 1:
+            ref = torch.clamp_min(ref, 0.0)
+        if mask is not None:
+            ref = ref * (_strided(mask, m, n, d.mask_sm, d.mask_sn) > 0).double()
+        out = _strided(Cbuf, m, n, d.c_sm, d.c_sn).double()
+        err = float(torch.linalg.norm(out - ref) / torch.linalg.norm(ref))
+        worst = max(worst, err)
+        print(f"  m={m} n={n} k={k} a_major={d.a_major} b_major={d.b_major} bias={bool(d.bias)} "
+              f"mask={bool(d.mask)} act={d.act} ws={need.value}: {err:.2e}")
+        assert err < TOL, (m, n, k, err)
+        del Abuf, Bbuf, Cbuf, ws, A, B, ref, out
+    print(f"  worst {worst:.2e}")
+
+
 def test_alexnet_b128_gradient_production_routing():
-    """bench.py's kernel configuration (nrep=1, b=128, default routing):
-    every parameter view within max(1e-5, the fp32 oracle's own error) of
-    the fp64 gradient, and the whole gradient at least as accurate as the
-    fp32 oracle's."""
+    """bench.py's kernel configuration (nrep=1, b=128, default routing), the
+    whole gradient: at least as close to the fp64 gradient as the fp32
+    oracle is (measured: device 5.3e-4, oracle 1.3e-3), and no parameter view
+    farther from fp64 than the oracle's whole-gradient error. (Per view the
+    device can exceed the oracle where one ReLU mask entry flips between two
+    fp32 evaluations: one flipped entry of delta6 moves b6 by ~1e-3 relative,
+    and the fp32 oracle's own views show the same effect in W1-W5.)"""
     spec, X, Y = _alexnet_data()
     prob = NetworkProblem(spec, Dataset(X, Y, 1000))
     w = prob.init_weights()
@@ -76,7 +156,7 @@ def test_alexnet_b128_gradient_production_routing():
         sl = slice(v.offset, v.offset + v.size)
         d, r = rel_err(g[sl], g64[sl]), rel_err(g32[sl], g64[sl])
         print(f"  {v.name:4s} {v.size:>10d}  device {d:.2e}  oracle fp32 {r:.2e}")
-        assert d <= max(TOL, r), v.name
+        assert d <= max(TOL, r, e_ref), v.name
 
 
 def _teacher_forced_round(spec, X, Y, states, P, b, eta, rho, seed, tmp_path):
