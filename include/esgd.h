@@ -253,6 +253,38 @@ int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* desc, esgd_stream_t stream);
  * same contract as esgd_gemm_ws_floats.                                    */
 int esgd_tc_gemm_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
 
+/* Implicit-GEMM convolution on the tensor cores (same 3xTF32 kernel): one
+ * GEMM operand is gathered by the kernel straight from a CNHW activation
+ * tensor (channel planes of `plane` floats, each [n][y][x] of src_h x
+ * src_w images) instead of an im2col matrix; the other operand, the output
+ * and the epilogue are those of `desc` (its `a` or `b` is ignored).
+ *   side 1 (forward / data gradient): A[m][k], m = pixel (n, r, c) of the
+ *     grid_h x grid_w grid (npix = images * grid_h * grid_w = desc->m),
+ *     k = (ch, kh, kw) in the packed weight order (desc->k = channels*kh*kw);
+ *   side 2 (weight gradient): B[n][k], n = (ch, kh, kw) (desc->n), k = pixel
+ *     (desc->k = npix).
+ * value = src[z*src_sb + ch*plane + n*src_h*src_w + y*src_w + x] with
+ * y = r*stride + yoff + sgn*kh, x = c*stride + xoff + sgn*kw, zero outside the
+ * image (zero padding). Convolution window (forward, weight gradient): sgn =
+ * +1, yoff = xoff = -pad. Data gradient of a stride-1 convolution: sgn = -1,
+ * yoff = xoff = +pad, src = the output gradient.
+ * (replaces network.py's dense contractions for the CNN layers the reference
+ * lacks — SPEC.md:67; oracle: oracle/esgd_oracle.py _im2col / _col2im)      */
+typedef struct {
+  const float* src; int64_t src_sb;
+  int32_t plane;
+  int32_t src_h, src_w;
+  int32_t grid_h, grid_w;
+  int32_t stride, yoff, xoff, sgn;
+  int32_t kh, kw;
+  int32_t npix;
+  int32_t channels;
+} esgd_conv_gather;
+int esgd_tc_conv_f32(const esgd_tc_gemm_desc* desc, const esgd_conv_gather* gather, int32_t side,
+                     esgd_stream_t stream);
+/* split-K workspace floats esgd_tc_conv_f32 needs for `desc` (0: no split). */
+int esgd_tc_conv_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
+
 /* activation forward/backward, kernels.py:30-70.
  * act_fwd: y = act(z); act_bwd: d = d * act'(z) (in place).                 */
 int esgd_act_fwd_f32(float* y, const float* z, int64_t n, int32_t act, esgd_stream_t stream);

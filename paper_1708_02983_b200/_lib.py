@@ -49,6 +49,15 @@ class TcGemmDesc(C.Structure):
     ]
 
 
+class ConvGather(C.Structure):
+    """esgd_conv_gather (include/esgd.h): the implicitly gathered operand."""
+    _fields_ = [
+        ("src", vp), ("src_sb", i64), ("plane", i32), ("src_h", i32), ("src_w", i32),
+        ("grid_h", i32), ("grid_w", i32), ("stride", i32), ("yoff", i32), ("xoff", i32), ("sgn", i32),
+        ("kh", i32), ("kw", i32), ("npix", i32), ("channels", i32),
+    ]
+
+
 class Tensor4(C.Structure):
     _fields_ = [("n", i32), ("c", i32), ("h", i32), ("w", i32),
                 ("sn", i64), ("sc", i64), ("sh", i64), ("sw", i64)]
@@ -102,6 +111,8 @@ _SIGS = {
     "esgd_gemm_f32": (C.c_int, [C.POINTER(GemmDesc), vp]),
     "esgd_tc_gemm_f32": (C.c_int, [C.POINTER(TcGemmDesc), vp]),
     "esgd_gemm_ws_floats": (C.c_int, [C.POINTER(GemmDesc), C.POINTER(i64)]),
+    "esgd_tc_conv_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
+    "esgd_tc_conv_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_tc_gemm_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_act_fwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),
     "esgd_act_bwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),

@@ -58,9 +58,13 @@ constexpr int kChunkKB = ESGD_CHUNK_KB;
 #endif
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR = false>
 struct Cfg {
-  static constexpr int kTileBytesB = BN * BK * 4;
+  // PAIR (cta_group::2): the CTA pair computes a 256 x BN tile; each CTA holds
+  // its own 128 A rows and half of B's BN rows in shared memory, and a 128 x BN
+  // accumulator in its own TMEM
+  static constexpr int kRowsB = PAIR ? BN / 2 : BN;
+  static constexpr int kTileBytesB = kRowsB * BK * 4;
   // stage layout: [lo spill | A raw | B raw], every tile 1024-B aligned.
   // In 3xTF32 mode A never gets a lo twin in smem: the split warps write the
   // tf32 hi/lo rows of A straight into TMEM and the MMAs read A from there —
@@ -87,7 +91,8 @@ struct Cfg {
   static constexpr int kTmemCols = SPLIT ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
   static_assert(!SPLIT || (kASlots >= 2 && kACol0 + 64 * kASlots <= 512), "TMEM budget");
   static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
-  static constexpr int kSmemBytes = kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*gathered B rows*/;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -182,6 +187,60 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_c, uint32_t tmem_a, ui
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_c),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum), "r"(0u));
 }
+// cta_group::2 (leader CTA issues for the pair; D / A rows 0-127 in the
+// leader's TMEM, 128-255 in the peer's; B halves in both CTAs' shared memory)
+__device__ __forceinline__ void mma_tf32_ts_pair(uint32_t tmem_c, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_c),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum), "r"(0u));
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_c, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_c),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(0u));
+}
+// commit the pair's outstanding MMAs to the barrier at the same offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the barrier at the same offset in CTA 0 of the cluster (the leader)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -248,6 +307,63 @@ struct Epi {
   int out_mode;     // 0 direct stores (via smem staging), 1 TMA store M-contiguous C, 2 TMA store N-contiguous C
   int m_fast;       // rasterise units m-fastest (M-contiguous output) else n-fastest
 };
+
+// Implicit-GEMM operand gathered by the split warps straight from a CNHW
+// activation tensor (channel planes of `plane` floats, each plane [n][y][x]
+// of images SH x SW), instead of a materialised im2col matrix:
+//   GM = 1 (conv forward / data gradient): A[m][k], m a pixel of the MH x MW
+//     grid (n, r, c), k = (ch, kh, kw) in the packed weight order;
+//   GM = 2 (weight gradient): B[n][k], n = (ch, kh, kw), k a pixel.
+// value = S[z*sb + ch*plane + n*SH*SW + y*SW + x] with
+//   y = r*stride + yoff + sgn*kh, x = c*stride + xoff + sgn*kw,
+// zero outside the image (padding) and for pixels / k beyond the problem.
+// sgn = +1 is the convolution's own window (forward, weight gradient); sgn =
+// -1 with stride 1 and offset +pad is the transposed window of the data
+// gradient (dx[ci][pix] = sum_{co,kh,kw} W[co][ci][kh][kw] d[co][pix+pad-k]).
+struct Gather {
+  const float* src;
+  int64_t sb;      // replica (batch) stride
+  int plane;       // channel plane pitch
+  int SH, SW;      // source image
+  int MH, MW;      // pixel grid of the gathered side
+  int stride, yoff, xoff, sgn;
+  int KH, KW;      // window
+  int npix;        // pixels of the grid over the whole batch of images
+  int kdim;        // channels * KH * KW
+};
+
+// (koff, kh | kw << 16) of packed k = (ch, kh, kw); an out-of-range k gets kh
+// = 0x7fff so every bounds test fails
+__device__ __forceinline__ void gather_k(const Gather& g, int k, int& koff, int& khkw) {
+  if (k >= g.kdim) {
+    koff = 0;
+    khkw = 0x7fff;
+    return;
+  }
+  const int kk = g.KH * g.KW;
+  const int ch = k / kk, t = k - ch * kk, kh = t / g.KW, kw = t - kh * g.KW;
+  koff = ch * g.plane + g.sgn * (kh * g.SW + kw);
+  khkw = kh | (kw << 16);
+}
+// pixel p of the grid -> offset of its window origin and the origin itself;
+// a pixel beyond the grid gets an origin far outside the image
+__device__ __forceinline__ void gather_pix(const Gather& g, int p, int& pbase, int& y0, int& x0) {
+  if (p >= g.npix) {
+    pbase = 0;
+    y0 = x0 = -(1 << 28);
+    return;
+  }
+  const int hw = g.MH * g.MW;
+  const int n = p / hw, rem = p - n * hw, r = rem / g.MW, c = rem - r * g.MW;
+  y0 = r * g.stride + g.yoff;
+  x0 = c * g.stride + g.xoff;
+  pbase = n * g.SH * g.SW + y0 * g.SW + x0;
+}
+__device__ __forceinline__ float gather_ld(const Gather& g, const float* zs, int pbase, int y0, int x0, int koff,
+                                           int khkw) {
+  const int y = y0 + g.sgn * (khkw & 0xffff), x = x0 + g.sgn * (khkw >> 16);
+  return ((unsigned)y < (unsigned)g.SH && (unsigned)x < (unsigned)g.SW) ? __ldg(zs + (pbase + koff)) : 0.f;
+}
 
 // epilogue value without the read-modify-write of accumulate (TMA-store path)
 __device__ __forceinline__ float epi_value(const Epi& ep, float x, int z, int row, int col) {
@@ -336,7 +452,8 @@ __device__ __forceinline__ void split_tile(uint32_t raw, uint32_t lo, int tid) {
 struct Unit {
   int n0, m0, z, slice, kb0, nkb;
 };
-__device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, int nkb_all, int BN_) {
+__device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, int nkb_all, int BN_,
+                                       int BM_ = BM) {
   Unit w;
   const int per_z = ntn * ntm * ep.splits;
   w.z = u / per_z;
@@ -349,9 +466,9 @@ __device__ __forceinline__ Unit unit_of(int u, const Epi& ep, int ntn, int ntm, 
   // 148 tiles over every page and throttled the stores to ~220 GB/s (TLB).
   if (ep.m_fast) {
     w.n0 = (r / ntm) * BN_;
-    w.m0 = (r % ntm) * BM;
+    w.m0 = (r % ntm) * BM_;
   } else {
-    w.m0 = (r / ntn) * BM;
+    w.m0 = (r / ntn) * BM_;
     w.n0 = (r % ntn) * BN_;
   }
   w.kb0 = w.slice * ep.kb_per_split;
@@ -436,55 +553,80 @@ __device__ unsigned long long g_trace[8][kTraceN];
   } while (0)
 #endif
 
-template <int BN, bool SPLIT, bool AMN, bool BMN>
+// PAIR = false: one CTA per 128 x BN output tile (cta_group::1).
+// PAIR = true: a cluster of two CTAs (one TPC) per 256 x BN tile
+// (cta_group::2): each CTA loads and splits its own 128 A rows and half of
+// B's rows, so every CTA's shared memory serves only half of B to the tensor
+// cores (the per-SM shared-memory traffic per MMA-cycle, which bounds the
+// 1-CTA kernel at BN = 128 / 192, drops by a third); the leader CTA's
+// single thread issues the pair's MMAs, whose commits arrive on both CTAs'
+// barriers (multicast); the peer's split and drain warps arrive on the
+// leader's barriers across the cluster.
+template <int BN, bool SPLIT, bool AMN, bool BMN, bool PAIR, int GM = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-              const __grid_constant__ CUtensorMap map_c, Epi ep) {
-  using C = Cfg<BN, SPLIT>;
+              const __grid_constant__ CUtensorMap map_c, Epi ep, Gather ga) {
+  using C = Cfg<BN, SPLIT, PAIR>;
+  static_assert(GM == 0 || (SPLIT && !AMN && !BMN), "gathered operands: 3xTF32, K-major partner");
+  constexpr int kCtas = PAIR ? 2 : 1;
+  constexpr int BMU = BM * kCtas;  // output rows per unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 32 KB, 1024-aligned
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + C::kStageOutBytes);
   // bars: full[S], split[S], empty[S], acc_full[2], acc_empty[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 2 * C::kAccBufs);
+  int2* btab = reinterpret_cast<int2*>(tmem_slot + 4);  // GM = 2: (koff, khkw) of this CTA's B rows
   const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
                  empty0 = smem_u32(bars + 2 * C::kStages), afull0 = smem_u32(bars + 3 * C::kStages),
                  aempty0 = afull0 + 8 * C::kAccBufs;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntn = (ep.n + BN - 1) / BN, ntm = (ep.m + BM - 1) / BM;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int ubase = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int ntn = (ep.n + BN - 1) / BN, ntm = (ep.m + BMU - 1) / BMU;
   const int nkb_all = (ep.k + BK - 1) / BK;
   const int nunits = ntn * ntm * ep.splits * ep.batch;
+  const int arow = (int)rank * BM;          // this CTA's first row inside a unit
+  const int brow = (int)rank * C::kRowsB;   // this CTA's first B row inside a unit
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(split0 + 8 * s, 4);  // one arrive per split warp
+      mbar_init(split0 + 8 * s, 4 * kCtas);  // one arrive per split warp (of both CTAs: the leader's is used)
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int b = 0; b < C::kAccBufs; ++b) {
       mbar_init(afull0 + 8 * b, 1);   // tcgen05.commit
-      mbar_init(aempty0 + 8 * b, kDrainWarps);  // one arrive per drain warp
+      mbar_init(aempty0 + 8 * b, kDrainWarps * kCtas);  // one arrive per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
+    if (lane == 0) {  // ---- TMA producer (each CTA its own A rows and B half)
       uint32_t g = 0;  // global k-block counter (stage ring position)
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+      for (int u = ubase; u < nunits; u += ustep) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
           if (g >= (uint32_t)C::kStages) mbar_wait(empty0 + 8 * s, ((g / C::kStages) - 1) & 1);
@@ -493,22 +635,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ESGD_X_NOTMA
           if (g >= (uint32_t)C::kStages) { mbar_arrive(full0 + 8 * s); continue; }
 #endif
-          mbar_expect_tx(full0 + 8 * s, kTileBytesA + C::kTileBytesB);
-          load_operand<AMN, BM>(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0, w.z);
-          load_operand<BMN, BN>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb, w.n0, w.z);
+          mbar_expect_tx(full0 + 8 * s, (GM == 1 ? 0 : kTileBytesA) + (GM == 2 ? 0 : C::kTileBytesB));
+          if (GM != 1)
+            load_operand<AMN, BM>(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0 + arow, w.z);
+          if (GM != 2)
+            load_operand<BMN, C::kRowsB>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb,
+                                         w.n0 + brow, w.z);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
-      constexpr uint32_t idesc = idesc_tf32(BM, BN, AMN, BMN);
-      constexpr uint32_t idesc_ts = idesc_tf32(BM, BN, false, BMN);  // A from TMEM is K-major
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer: one K-chunk per TMEM accumulator buffer
+      constexpr uint32_t idesc = idesc_tf32(BMU, BN, AMN, BMN);
+      constexpr uint32_t idesc_ts = idesc_tf32(BMU, BN, false, BMN);  // A from TMEM is K-major
       uint32_t g = 0, c = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+      for (int u = ubase; u < nunits; u += ustep) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
         for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
           const int buf = c % C::kAccBufs;
-          if (c >= (uint32_t)C::kAccBufs) mbar_wait(aempty0 + 8 * buf, ((c / C::kAccBufs) - 1) & 1);
+          if (c >= (uint32_t)C::kAccBufs) {
+            if (PAIR) mbar_wait_cluster(aempty0 + 8 * buf, ((c / C::kAccBufs) - 1) & 1);
+            else mbar_wait(aempty0 + 8 * buf, ((c / C::kAccBufs) - 1) & 1);
+          }
           TRACE(2, c);
           tc_fence_after();
           const uint32_t acc = tmem + buf * BN;
@@ -516,11 +664,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = kc; kb < kend; ++kb, ++g) {
             const int s = g % C::kStages;
             const uint32_t ph = (g / C::kStages) & 1;
-            if (SPLIT) mbar_wait(split0 + 8 * s, ph);
-            else mbar_wait(full0 + 8 * s, ph);
+            if (SPLIT) {
+              if (PAIR) mbar_wait_cluster(split0 + 8 * s, ph);
+              else mbar_wait(split0 + 8 * s, ph);
+            } else {
+              mbar_wait(full0 + 8 * s, ph);
+            }
             TRACE(1, g);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + s * C::kStageBytes);
+#ifndef ESGD_X_NOMMA
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               // K-major: 8 tf32 = 32 B along K inside the swizzle atom;
@@ -530,16 +683,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (SPLIT) {
                 const uint64_t bl = op_desc<BMN>(st + C::kOffBLo, kk);
                 const uint32_t ahi = tmem + C::kACol0 + (g % C::kASlots) * 64 + kk * 8, alo = ahi + 32;
-                mma_tf32_ts(acc, alo, bh, idesc_ts, acc0);  // small terms first
-                mma_tf32_ts(acc, ahi, bl, idesc_ts, 1u);
-                mma_tf32_ts(acc, ahi, bh, idesc_ts, 1u);
+                if (PAIR) {
+                  mma_tf32_ts_pair(acc, alo, bh, idesc_ts, acc0);  // small terms first
+                  mma_tf32_ts_pair(acc, ahi, bl, idesc_ts, 1u);
+                  mma_tf32_ts_pair(acc, ahi, bh, idesc_ts, 1u);
+                } else {
+                  mma_tf32_ts(acc, alo, bh, idesc_ts, acc0);  // small terms first
+                  mma_tf32_ts(acc, ahi, bl, idesc_ts, 1u);
+                  mma_tf32_ts(acc, ahi, bh, idesc_ts, 1u);
+                }
               } else {
-                mma_tf32(acc, op_desc<AMN>(st + C::kOffA, kk), bh, idesc, acc0);
+                if (PAIR) mma_tf32_pair(acc, op_desc<AMN>(st + C::kOffA, kk), bh, idesc, acc0);
+                else mma_tf32(acc, op_desc<AMN>(st + C::kOffA, kk), bh, idesc, acc0);
               }
             }
-            mma_commit(empty0 + 8 * s);  // slot reusable once these MMAs retire
+#endif
+            if (PAIR) mma_commit_pair(empty0 + 8 * s);  // slot reusable (in both CTAs) once these MMAs retire
+            else mma_commit(empty0 + 8 * s);
           }
-          mma_commit(afull0 + 8 * buf);  // this chunk's partial sum is complete
+          if (PAIR) mma_commit_pair(afull0 + 8 * buf);  // this chunk's partial sum is complete
+          else mma_commit(afull0 + 8 * buf);
         }
       }
     }
@@ -550,8 +713,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int et = threadIdx.x - 64;  // 0..127
       const int q = warp & 3, r = q * 32 + lane;
       uint32_t g = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+      for (int u = ubase; u < nunits; u += ustep) {
+        const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
+        const float* zs = GM ? ga.src + (int64_t)w.z * ga.sb : nullptr;
+        int pb = 0, py0 = 0, px0 = 0;  // GM = 1: this thread's row (a pixel of the M grid)
+        if (GM == 1) gather_pix(ga, w.m0 + arow + r, pb, py0, px0);
+        if (GM == 2) {  // (koff, kh|kw) of this CTA's B rows, once per unit
+          named_bar_sync(3, 128);  // the previous unit's last k-block no longer reads the table
+          for (int i = et; i < C::kRowsB; i += 128) {
+            int ko, kw;
+            gather_k(ga, w.n0 + brow + i < ep.n ? w.n0 + brow + i : ga.kdim, ko, kw);
+            btab[i] = make_int2(ko, kw);
+          }
+          named_bar_sync(3, 128);
+        }
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
@@ -559,7 +734,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           const uint32_t sa = st + C::kOffA;
           uint32_t hi[32], lo[32];
-          if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
+          if (GM == 1) {  // A row r gathered from the activations (implicit im2col)
+            int ko, kk;
+            gather_k(ga, (w.kb0 + kb) * BK + lane, ko, kk);
+            float xv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              xv[j] = gather_ld(ga, zs, pb, py0, px0, __shfl_sync(0xffffffffu, ko, j),
+                                __shfl_sync(0xffffffffu, kk, j));
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float h = tf32_hi(xv[j]);
+              hi[j] = __float_as_uint(h);
+              lo[j] = __float_as_uint(__fsub_rn(xv[j], h));
+            }
+          } else if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const float4 x = lds4(sa + r * 128 + ((c ^ (r & 7)) << 4));
@@ -598,13 +787,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           // every split thread has read its A row: B lo may overwrite the tile
           named_bar_sync(3, 128);
 #ifndef ESGD_X_NOSPLITB
-          split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
+          if (GM == 2) {
+            // B rows gathered from the activations: lane = pixel (coalesced),
+            // raw value (= B_hi to the tensor core) and lo into the SW128 rows
+            int pb2, y02, x02;
+            gather_pix(ga, (w.kb0 + kb) * BK + lane, pb2, y02, x02);
+            const uint32_t col = ((lane & 3) << 2);
+            for (int i = warp - 2; i < C::kRowsB; i += 4) {
+              const int2 t = btab[i];
+              const float v = gather_ld(ga, zs, pb2, y02, x02, t.x, t.y);
+              const uint32_t off = i * 128 + ((((lane >> 2) ^ (i & 7))) << 4) + col;
+              const float h = tf32_hi(v);
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + C::kOffB + off), "f"(v) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + C::kOffBLo + off), "f"(__fsub_rn(v, h)) : "memory");
+            }
+          } else {
+            split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
+          }
 #endif
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(split0 + 8 * s);
+          if (lane == 0) {
+            if (PAIR) mbar_arrive_leader(split0 + 8 * s);
+            else mbar_arrive(split0 + 8 * s);
+          }
           if (warp == 2 && lane == 0) TRACE(4, g);
         }
       }
@@ -621,8 +829,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3, h = (warp - 6) >> 2;
     const int issuer = 192 + h * 128;  // lane 0 of warp 6 / warp 10: bulk-store issue
     uint32_t c = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN);
+    for (int u = ubase; u < nunits; u += ustep) {
+      const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
       float racc[HB];
 #pragma unroll
       for (int j = 0; j < HB; ++j) racc[j] = 0.f;
@@ -653,10 +861,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(aempty0 + 8 * buf);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_leader(aempty0 + 8 * buf);
+          else mbar_arrive(aempty0 + 8 * buf);
+        }
         if (warp == 6 && lane == 0) TRACE(6, c);
       }
-      const int row = w.m0 + q * 32 + lane;
+      const int m0 = w.m0 + arow;  // this CTA's rows of the unit
+      const int row = m0 + q * 32 + lane;
       const int n0 = w.n0 + h * HB;  // first column of this warp's half
 #ifdef ESGD_X_NOEPI
       if (row == -1) {
@@ -705,13 +917,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(w.m0), "r"(col0), "r"(w.z), "r"(sb)
+                  "r"(m0), "r"(col0), "r"(w.z), "r"(sb)
                   : "memory");
             else
               asm volatile(
                   "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                       reinterpret_cast<uint64_t>(&map_c)),
-                  "r"(col0), "r"(w.m0), "r"(w.z), "r"(sb)
+                  "r"(col0), "r"(m0), "r"(w.z), "r"(sb)
                   : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -722,10 +934,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer's remote arrives / the leader's commits are done
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
   }
 }
 
@@ -797,9 +1013,18 @@ inline int pick_bn(int64_t m, int64_t n, bool split) {
   if (padded(n, 192) < padded(n, 128)) return 192;
   return (padded(n, 192) == padded(n, 128) && m >= 16 * BM) ? 192 : 128;
 }
-// padded MMA area of an orientation (M tiled by 128, N by the chosen width)
+// CTA-pair mode (cta_group::2, 256-row units) for the 3xTF32 path when M has
+// enough rows that 256-row tiles add little padding (ESGD_TC_PAIR=0/1 forces
+// it off / on for tuning runs)
+inline bool use_pair(int64_t m, bool split) {
+  static const int force = getenv("ESGD_TC_PAIR") ? atoi(getenv("ESGD_TC_PAIR")) : -1;
+  if (!split || m <= BM) return false;
+  if (force >= 0) return force == 1;
+  return m >= 8 * 256 && padded(m, 256) * 8 <= padded(m, BM) * 9;
+}
+// padded MMA area of an orientation (M tiled by 128 or 256, N by the chosen width)
 inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
-  return padded(m, BM) * padded(n, pick_bn(m, n, split));
+  return padded(m, use_pair(m, split) ? 2 * BM : BM) * padded(n, pick_bn(m, n, split));
 }
 
 // Launch plan of one GEMM: orientation (C^T = B.A^T when it needs less padded
@@ -807,9 +1032,10 @@ inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
 struct Plan {
   esgd_tc_gemm_desc d;  // the oriented problem
   int bn, splits, kbps;
+  bool pair;            // cta_group::2, 256-row units
 };
 
-inline Plan make_plan(const esgd_tc_gemm_desc* d0) {
+inline Plan make_plan(const esgd_tc_gemm_desc* d0, bool allow_swap = true) {
   Plan p;
   p.d = *d0;
   const bool split = d0->precision == 3;
@@ -817,7 +1043,7 @@ inline Plan make_plan(const esgd_tc_gemm_desc* d0) {
   // swapped; take it when it needs less padded tensor-core work (M is tiled
   // by 128: a 64- or 192-row M wastes half / a quarter of every MMA). Only
   // without a per-column bias (the epilogue applies bias along N).
-  if (!d0->bias && padded_cost(d0->n, d0->m, split) < padded_cost(d0->m, d0->n, split)) {
+  if (allow_swap && !d0->bias && padded_cost(d0->n, d0->m, split) < padded_cost(d0->m, d0->n, split)) {
     esgd_tc_gemm_desc& sw = p.d;
     sw.m = d0->n; sw.n = d0->m;
     sw.a = d0->b; sw.lda = d0->ldb; sw.a_sb = d0->b_sb; sw.a_major = d0->b_major;
@@ -827,6 +1053,8 @@ inline Plan make_plan(const esgd_tc_gemm_desc* d0) {
   }
   const esgd_tc_gemm_desc* d = &p.d;
   p.bn = pick_bn(d->m, d->n, split);
+  p.pair = use_pair(d->m, split);
+  const int bmu = p.pair ? 2 * BM : BM, units_per_wave = p.pair ? kNumSMs / 2 : kNumSMs;
   const int nkb = (d->k + BK - 1) / BK;
   // The K split depends on the per-replica problem only, never on `batch` or
   // on the workspace size: a replica computes bit-identical results however
@@ -837,10 +1065,10 @@ inline Plan make_plan(const esgd_tc_gemm_desc* d0) {
   // the partials for k_tc_reduce; 3-4 far worse). A NULL workspace means "do
   // not split"; a workspace that is too small is an error (esgd_tc_gemm_f32
   // returns ESGD_ERR_UNSUPPORTED; size it with esgd_tc_gemm_ws_floats).
-  const int tiles_z = ((d->n + p.bn - 1) / p.bn) * ((d->m + BM - 1) / BM);
+  const int tiles_z = ((d->n + p.bn - 1) / p.bn) * ((d->m + bmu - 1) / bmu);
   int splits = 1;
-  if (d->ws && tiles_z < kNumSMs && nkb >= 2 * kChunkKB) {
-    splits = (ESGD_SPLIT_WAVES * kNumSMs) / tiles_z;
+  if (d->ws && tiles_z < units_per_wave && nkb >= 2 * kChunkKB) {
+    splits = (ESGD_SPLIT_WAVES * units_per_wave) / tiles_z;
     splits = std::min(splits, nkb / (2 * kChunkKB));
     splits = std::min(splits, 128);
     if (splits < 1) splits = 1;
@@ -856,22 +1084,30 @@ inline int64_t ws_need(const Plan& p) {
   return p.splits > 1 ? (int64_t)p.splits * p.d.m * p.d.n * p.d.batch : 0;
 }
 
-template <int BN, bool SPLIT, bool AMN, bool BMN>
-int launch(const Plan& p, cudaStream_t st) {
-  using C = Cfg<BN, SPLIT>;
+template <int BN, bool SPLIT, bool AMN, bool BMN, bool PAIR, int GM = 0>
+int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
+  using C = Cfg<BN, SPLIT, PAIR>;
+  constexpr int BMU = PAIR ? 2 * BM : BM;
   const esgd_tc_gemm_desc* d = &p.d;
   // per-device attribute; cheap, and legal while a stream is being captured
-  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT, AMN, BMN>,
+  cudaError_t e = cudaFuncSetAttribute(k_tc_gemm<BN, SPLIT, AMN, BMN, PAIR, GM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: smem attribute: %s", cudaGetErrorString(e));
   CUtensorMap ma, mb;
   // 3xTF32: A is read by the split warps (not by UMMA), plain 128B swizzle
-  int rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN, /*atom32=*/!SPLIT);
-  if (rc) return rc;
-  rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, BN, BMN);
-  if (rc) return rc;
+  memset(&ma, 0, sizeof(ma));
+  memset(&mb, 0, sizeof(mb));
+  int rc = ESGD_OK;
+  if (GM != 1) {  // (a gathered operand has no tensor map)
+    rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN, /*atom32=*/!SPLIT);
+    if (rc) return rc;
+  }
+  if (GM != 2) {
+    rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, C::kRowsB, BMN);
+    if (rc) return rc;
+  }
   const int splits = p.splits, kbps = p.kbps;
-  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BM - 1) / BM) * d->batch;
+  const int tiles = ((d->n + BN - 1) / BN) * ((d->m + BMU - 1) / BMU) * d->batch;
   // output: TMA store when one C stride is unit and the other 16-B aligned
   int out_mode = 0;
   CUtensorMap mc;
@@ -900,10 +1136,30 @@ int launch(const Plan& p, cudaStream_t st) {
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
          d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch, out_mode,
          m_fast};
-  // persistent: one CTA per SM (smem-limited), units dealt round-robin
+  // persistent: one CTA per SM (smem-limited), units dealt round-robin (to
+  // CTA pairs in PAIR mode: clusters of 2 on one TPC)
   const int64_t units = (int64_t)tiles * splits;
-  const int grid = (int)std::min<int64_t>(units, kNumSMs);
-  k_tc_gemm<BN, SPLIT, AMN, BMN><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, ep);
+  if (PAIR) {
+    const int pairs = (int)std::min<int64_t>(units, kNumSMs / 2);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_tc_gemm<BN, SPLIT, AMN, BMN, true, GM>, ma, mb, mc, ep, ga);
+    ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: cluster launch: %s", cudaGetErrorString(e));
+  } else {
+    const int grid = (int)std::min<int64_t>(units, kNumSMs);
+    k_tc_gemm<BN, SPLIT, AMN, BMN, false, GM><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, ep, ga);
+  }
   if (splits > 1) {
     dim3 rg(stride_grid((int64_t)d->m * d->n, 256, 8), d->batch);
     k_tc_reduce<<<rg, 256, 0, st>>>(ep);
@@ -911,11 +1167,21 @@ int launch(const Plan& p, cudaStream_t st) {
   return check_launch("esgd_tc_gemm_f32");
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR>
 int launch_major(const Plan& p, cudaStream_t st) {
   const esgd_tc_gemm_desc* d = &p.d;
-  if (d->a_major) return d->b_major ? launch<BN, SPLIT, true, true>(p, st) : launch<BN, SPLIT, true, false>(p, st);
-  return d->b_major ? launch<BN, SPLIT, false, true>(p, st) : launch<BN, SPLIT, false, false>(p, st);
+  if (d->a_major)
+    return d->b_major ? launch<BN, SPLIT, true, true, PAIR>(p, st) : launch<BN, SPLIT, true, false, PAIR>(p, st);
+  return d->b_major ? launch<BN, SPLIT, false, true, PAIR>(p, st) : launch<BN, SPLIT, false, false, PAIR>(p, st);
+}
+template <int BN>
+int launch_split(const Plan& p, cudaStream_t st) {
+  return p.pair ? launch_major<BN, true, true>(p, st) : launch_major<BN, true, false>(p, st);
+}
+// implicit-GEMM convolutions: GM = 1 gathers A (K-major B), GM = 2 gathers B (K-major A)
+template <int BN, int GM>
+int launch_gather(const Plan& p, cudaStream_t st, const Gather& ga) {
+  return p.pair ? launch<BN, true, false, false, true, GM>(p, st, ga) : launch<BN, true, false, false, false, GM>(p, st, ga);
 }
 
 int validate(const esgd_tc_gemm_desc* d) {
@@ -963,9 +1229,70 @@ extern "C" int esgd_tc_gemm_f32(const esgd_tc_gemm_desc* d, esgd_stream_t stream
   ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
                "tc_gemm: split-K workspace too small (need %lld floats, have %lld; size it with "
                "esgd_tc_gemm_ws_floats)", (long long)need, (long long)d->ws_floats);
-  if (p.bn == 64) return split ? tc::launch_major<64, true>(p, st) : tc::launch_major<64, false>(p, st);
-  if (p.bn == 192) return tc::launch_major<192, true>(p, st);
-  return split ? tc::launch_major<128, true>(p, st) : tc::launch_major<128, false>(p, st);
+  if (p.bn == 64) return split ? tc::launch_split<64>(p, st) : tc::launch_major<64, false, false>(p, st);
+  if (p.bn == 192) return tc::launch_split<192>(p, st);
+  return split ? tc::launch_split<128>(p, st) : tc::launch_major<128, false, false>(p, st);
+}
+
+extern "C" int esgd_tc_conv_f32(const esgd_tc_gemm_desc* d, const esgd_conv_gather* cg, int32_t side,
+                                esgd_stream_t stream) {
+  using namespace esgd;
+  if (int rc = tc::validate(d)) return rc;
+  ESGD_REQUIRE(cg && (side == 1 || side == 2), ESGD_ERR_INPUT, "tc_conv: gather descriptor and side 1|2 required");
+  ESGD_REQUIRE(d->precision == 3, ESGD_ERR_UNSUPPORTED, "tc_conv: 3xTF32 only");
+  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
+  const int64_t kdim = (int64_t)cg->channels * cg->kh * cg->kw;
+  ESGD_REQUIRE(cg->src && cg->kh >= 1 && cg->kw >= 1 && cg->channels >= 1 && cg->stride >= 1 &&
+                   (cg->sgn == 1 || cg->sgn == -1) && cg->src_h >= 1 && cg->src_w >= 1 && cg->grid_h >= 1 &&
+                   cg->grid_w >= 1 && cg->npix >= 1 && cg->npix % (cg->grid_h * cg->grid_w) == 0 &&
+                   (int64_t)cg->plane >= (int64_t)(cg->npix / (cg->grid_h * cg->grid_w)) * cg->src_h * cg->src_w,
+               ESGD_ERR_INPUT, "tc_conv: bad gather geometry");
+  ESGD_REQUIRE((int64_t)cg->plane * cg->channels < (int64_t(1) << 31) && kdim < (int64_t(1) << 30),
+               ESGD_ERR_UNSUPPORTED, "tc_conv: source tensor too large for 32-bit offsets");
+  if (side == 1) {
+    ESGD_REQUIRE(d->m == cg->npix && d->k == kdim, ESGD_ERR_SHAPE,
+                 "tc_conv: gathered A is npix x channels*kh*kw (m=%d k=%d vs %d x %lld)", d->m, d->k, cg->npix,
+                 (long long)kdim);
+    ESGD_REQUIRE(d->b && d->b_major == 0 && (d->ldb & 3) == 0 && d->ldb >= d->k && aligned16(d->b),
+                 ESGD_ERR_SHAPE, "tc_conv: B must be K-major with a 16-B aligned pitch");
+  } else {
+    ESGD_REQUIRE(d->n == kdim && d->k == cg->npix, ESGD_ERR_SHAPE,
+                 "tc_conv: gathered B is channels*kh*kw x npix (n=%d k=%d vs %lld x %d)", d->n, d->k,
+                 (long long)kdim, cg->npix);
+    ESGD_REQUIRE(d->a && d->a_major == 0 && (d->lda & 3) == 0 && d->lda >= d->k && aligned16(d->a),
+                 ESGD_ERR_SHAPE, "tc_conv: A must be K-major with a 16-B aligned pitch");
+  }
+  ESGD_REQUIRE(d->c, ESGD_ERR_INPUT, "tc_conv: null output");
+  ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
+               "tc_conv: batch strides must be multiples of 4");
+  tc::Gather ga{cg->src, cg->src_sb, cg->plane, cg->src_h, cg->src_w, cg->grid_h, cg->grid_w, cg->stride,
+                cg->yoff, cg->xoff, cg->sgn, cg->kh, cg->kw, cg->npix, (int)kdim};
+  const tc::Plan p = tc::make_plan(d, /*allow_swap=*/false);
+  const int64_t need = tc::ws_need(p);
+  ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
+               "tc_conv: split-K workspace too small (need %lld floats, have %lld; size it with "
+               "esgd_tc_conv_ws_floats)", (long long)need, (long long)d->ws_floats);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (side == 1) {
+    if (p.bn == 64) return tc::launch_gather<64, 1>(p, st, ga);
+    if (p.bn == 192) return tc::launch_gather<192, 1>(p, st, ga);
+    return tc::launch_gather<128, 1>(p, st, ga);
+  }
+  if (p.bn == 64) return tc::launch_gather<64, 2>(p, st, ga);
+  if (p.bn == 192) return tc::launch_gather<192, 2>(p, st, ga);
+  return tc::launch_gather<128, 2>(p, st, ga);
+}
+
+extern "C" int esgd_tc_conv_ws_floats(const esgd_tc_gemm_desc* d, int64_t* floats) {
+  using namespace esgd;
+  ESGD_REQUIRE(floats, ESGD_ERR_INPUT, "tc_conv_ws_floats: null output");
+  *floats = 0;
+  if (int rc = tc::validate(d)) return rc;
+  if (d->m == 0 || d->n == 0 || d->batch == 0 || d->k == 0) return ESGD_OK;
+  esgd_tc_gemm_desc q = *d;
+  if (!q.ws) q.ws = reinterpret_cast<float*>(uintptr_t(256));
+  *floats = tc::ws_need(tc::make_plan(&q, /*allow_swap=*/false));
+  return ESGD_OK;
 }
 
 #ifdef ESGD_TRACE
