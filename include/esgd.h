@@ -263,7 +263,7 @@ int esgd_tc_gemm_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
  *     k = (ch, kh, kw) in the packed weight order (desc->k = channels*kh*kw);
  *   side 2 (weight gradient): B[n][k], n = (ch, kh, kw) (desc->n), k = pixel
  *     (desc->k = npix).
- * value = src[z*src_sb + ch*plane + n*src_h*src_w + y*src_w + x] with
+ * value = src[z*src_sb + ch*plane + n*img_stride + y*src_w + x] with
  * y = r*stride + yoff + sgn*kh, x = c*stride + xoff + sgn*kw, zero outside the
  * image (zero padding). Convolution window (forward, weight gradient): sgn =
  * +1, yoff = xoff = -pad. Data gradient of a stride-1 convolution: sgn = -1,
@@ -272,7 +272,8 @@ int esgd_tc_gemm_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
  * lacks — SPEC.md:67; oracle: oracle/esgd_oracle.py _im2col / _col2im)      */
 typedef struct {
   const float* src; int64_t src_sb;
-  int32_t plane;
+  int32_t plane;      /* channel stride (floats) */
+  int32_t img_stride; /* image stride: 0 = src_h*src_w (CNHW planes); c*h*w for NCHW rows */
   int32_t src_h, src_w;
   int32_t grid_h, grid_w;
   int32_t stride, yoff, xoff, sgn;

@@ -52,7 +52,7 @@ class TcGemmDesc(C.Structure):
 class ConvGather(C.Structure):
     """esgd_conv_gather (include/esgd.h): the implicitly gathered operand."""
     _fields_ = [
-        ("src", vp), ("src_sb", i64), ("plane", i32), ("src_h", i32), ("src_w", i32),
+        ("src", vp), ("src_sb", i64), ("plane", i32), ("img_stride", i32), ("src_h", i32), ("src_w", i32),
         ("grid_h", i32), ("grid_w", i32), ("stride", i32), ("yoff", i32), ("xoff", i32), ("sgn", i32),
         ("kh", i32), ("kw", i32), ("npix", i32), ("channels", i32),
     ]

@@ -58,7 +58,7 @@ constexpr int kChunkKB = ESGD_CHUNK_KB;
 #endif
 constexpr int kTileBytesA = BM * BK * 4;  // 16 KB
 
-template <int BN, bool SPLIT, bool PAIR = false>
+template <int BN, bool SPLIT, bool PAIR = false, int EXTRA = 0>
 struct Cfg {
   // PAIR (cta_group::2): the CTA pair computes a 256 x BN tile; each CTA holds
   // its own 128 A rows and half of B's BN rows in shared memory, and a 128 x BN
@@ -78,7 +78,9 @@ struct Cfg {
   static constexpr int kOffB = kOffA + kTileBytesA;
   static constexpr int kOffBLo = 0;
   static constexpr int kStageBytes = kLoSpill + kTileBytesA + kTileBytesB;
-  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
+  // EXTRA: bytes after the barriers (the gathered-B row table of GM = 2)
+  static constexpr int kStages =
+      (192 * 1024 - EXTRA) / kStageBytes > 8 ? 8 : (192 * 1024 - EXTRA) / kStageBytes;
 #ifndef ESGD_ACC_BUFS128
 #define ESGD_ACC_BUFS128 2
 #endif
@@ -92,7 +94,7 @@ struct Cfg {
   static_assert(!SPLIT || (kASlots >= 2 && kACol0 + 64 * kASlots <= 512), "TMEM budget");
   static constexpr int kStageOutBytes = 32768;  // epilogue staging: 128 rows x 64 cols fp32
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*gathered B rows*/;
+      kStages * kStageBytes + kStageOutBytes + 1024 /*align*/ + 256 /*barriers*/ + EXTRA;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -324,13 +326,31 @@ struct Gather {
   const float* src;
   int64_t sb;      // replica (batch) stride
   int plane;       // channel plane pitch
+  int nstride;     // image stride (SH*SW for CNHW planes, C*SH*SW for NCHW rows)
   int SH, SW;      // source image
   int MH, MW;      // pixel grid of the gathered side
   int stride, yoff, xoff, sgn;
   int KH, KW;      // window
   int npix;        // pixels of the grid over the whole batch of images
   int kdim;        // channels * KH * KW
+  int hpitch;      // GM = 3: floats per channel of the smem halo
 };
+
+// GM = 3 (halo): the source rows a unit's 128 pixels touch, as flattened
+// (image, y) rows of the channel planes, clamped to the planes
+__device__ __forceinline__ void halo_rows(const Gather& g, int m0, int& r_lo, int& r_hi) {
+  const int hw = g.MH * g.MW, last = min(m0 + BM, g.npix) - 1;
+  const int n0 = m0 / hw, y0 = ((m0 - n0 * hw) / g.MW) * g.stride + g.yoff;
+  const int n1 = last / hw, y1 = ((last - n1 * hw) / g.MW) * g.stride + g.yoff;
+  const int reach = g.sgn * (g.KH - 1);
+  r_lo = max(0, n0 * g.SH + y0 + min(0, reach));
+  r_hi = min(g.npix / hw * g.SH - 1, n1 * g.SH + y1 + max(0, reach));
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const float* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 
 // (koff, kh | kw << 16) of packed k = (ch, kh, kw); an out-of-range k gets kh
 // = 0x7fff so every bounds test fails
@@ -357,12 +377,26 @@ __device__ __forceinline__ void gather_pix(const Gather& g, int p, int& pbase, i
   const int n = p / hw, rem = p - n * hw, r = rem / g.MW, c = rem - r * g.MW;
   y0 = r * g.stride + g.yoff;
   x0 = c * g.stride + g.xoff;
-  pbase = n * g.SH * g.SW + y0 * g.SW + x0;
+  pbase = n * g.nstride + y0 * g.SW + x0;
 }
 __device__ __forceinline__ float gather_ld(const Gather& g, const float* zs, int pbase, int y0, int x0, int koff,
                                            int khkw) {
   const int y = y0 + g.sgn * (khkw & 0xffff), x = x0 + g.sgn * (khkw >> 16);
   return ((unsigned)y < (unsigned)g.SH && (unsigned)x < (unsigned)g.SW) ? __ldg(zs + (pbase + koff)) : 0.f;
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+// cp.async of one gathered element (zero-filled when outside the image)
+__device__ __forceinline__ void gather_cp(const Gather& g, const float* zs, int pbase, int y0, int x0, int koff,
+                                          int khkw, uint32_t dst) {
+  const int y = y0 + g.sgn * (khkw & 0xffff), x = x0 + g.sgn * (khkw >> 16);
+  const bool ok = (unsigned)y < (unsigned)g.SH && (unsigned)x < (unsigned)g.SW;
+  cp_async4(dst, ok ? zs + (pbase + koff) : zs, ok);
 }
 
 // epilogue value without the read-modify-write of accumulate (TMA-store path)
@@ -576,7 +610,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + C::kStageOutBytes);
   // bars: full[S], split[S], empty[S], acc_full[2], acc_empty[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::kStages + 2 * C::kAccBufs);
-  int2* btab = reinterpret_cast<int2*>(tmem_slot + 4);  // GM = 2: (koff, khkw) of this CTA's B rows
   const uint32_t full0 = smem_u32(bars), split0 = smem_u32(bars + C::kStages),
                  empty0 = smem_u32(bars + 2 * C::kStages), afull0 = smem_u32(bars + 3 * C::kStages),
                  aempty0 = afull0 + 8 * C::kAccBufs;
@@ -595,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(full0 + 8 * s, 1);
+      mbar_init(full0 + 8 * s, (GM == 1 || GM == 2) ? 1 + 128 : 1);  // + the 128 gathering threads (cp.async arrive)
       mbar_init(split0 + 8 * s, 4 * kCtas);  // one arrive per split warp (of both CTAs: the leader's is used)
       mbar_init(empty0 + 8 * s, 1);
     }
@@ -635,8 +668,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ESGD_X_NOTMA
           if (g >= (uint32_t)C::kStages) { mbar_arrive(full0 + 8 * s); continue; }
 #endif
-          mbar_expect_tx(full0 + 8 * s, (GM == 1 ? 0 : kTileBytesA) + (GM == 2 ? 0 : C::kTileBytesB));
-          if (GM != 1)
+          if (GM == 3) {  // halo: the channels this k-block touches, rows of the unit, one bulk copy each
+            int r_lo, r_hi;
+            halo_rows(ga, w.m0 + arow, r_lo, r_hi);
+            const int k0 = (w.kb0 + kb) * BK, kk = ga.KH * ga.KW;
+            const int c_lo = k0 / kk, c_hi = min(k0 + BK, ga.kdim) / kk - ((min(k0 + BK, ga.kdim) % kk) ? 0 : 1);
+            const int e0 = r_lo * ga.SW, e0a = e0 & ~3;
+            const int len = min((e0 - e0a + (r_hi - r_lo + 1) * ga.SW + 3) & ~3, ga.plane - e0a);
+            mbar_expect_tx(full0 + 8 * s, C::kTileBytesB + (uint32_t)(c_hi - c_lo + 1) * len * 4);
+            const float* zs = ga.src + (int64_t)w.z * ga.sb;
+            for (int c = c_lo; c <= c_hi; ++c)
+              bulk_g2s(smem_u32(st + C::kOffA) + (c - c_lo) * ga.hpitch * 4, zs + (int64_t)c * ga.plane + e0a,
+                       len * 4, full0 + 8 * s);
+          } else {
+            mbar_expect_tx(full0 + 8 * s, (GM == 1 ? 0 : kTileBytesA) + (GM == 2 ? 0 : C::kTileBytesB));
+          }
+          if (GM == 0 || GM == 2)
             load_operand<AMN, BM>(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0 + arow, w.z);
           if (GM != 2)
             load_operand<BMN, C::kRowsB>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb,
@@ -713,42 +760,108 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int et = threadIdx.x - 64;  // 0..127
       const int q = warp & 3, r = q * 32 + lane;
       uint32_t g = 0;
+      // Gathered operand (GM): the split warps also produce it, kAhead
+      // k-blocks ahead of the split, with 4-byte cp.async (zero-fill for the
+      // padding) into the stage's raw tile in the TMA layout (K-major SW128),
+      // arriving on the stage's full barrier — loads in flight without
+      // holding registers. GM = 1: row r = pixel (lane-consecutive pixels:
+      // coalesced), 32 k; GM = 2: B rows n of this CTA, lane = pixel.
+      constexpr int kAhead = (GM == 1 || GM == 2) ? (C::kStages - 2 < 3 ? C::kStages - 2 : 3) : 0;
+      int gu = ubase, gkb = 0;  // gather cursor: unit, k-block in unit
+      uint32_t gg = 0;          // global k-block counter of the cursor
+      Unit gw = unit_of(gu < nunits ? gu : 0, ep, ntn, ntm, nkb_all, BN, BMU);
+      int gpb = 0, gy0 = 0, gx0 = 0;  // GM = 1: this thread's pixel in the cursor's unit
+      // GM = 2: (koff, kh|kw) of the warp's B rows i = warp-2 + 4j, j = lane and lane + 32
+      int gk[2] = {0, 0}, gkk[2] = {0, 0};
+      auto unit_rows = [&]() {
+        if (GM == 1) gather_pix(ga, gw.m0 + arow + r, gpb, gy0, gx0);
+        if (GM == 2) {
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = warp - 2 + 4 * (lane + 32 * h2), n = gw.n0 + brow + i;
+            gather_k(ga, (i < C::kRowsB && n < ep.n) ? n : ga.kdim, gk[h2], gkk[h2]);
+          }
+        }
+      };
+      if ((GM == 1 || GM == 2) && gu < nunits) unit_rows();
+      auto gather_next = [&]() {
+        if (gu >= nunits) return;
+        const int s2 = gg % C::kStages;
+        if (gg >= (uint32_t)C::kStages) mbar_wait(empty0 + 8 * s2, ((gg / C::kStages) - 1) & 1);
+        const uint32_t st2 = smem_u32(smem + s2 * C::kStageBytes);
+        const float* zs = ga.src + (int64_t)gw.z * ga.sb;
+        if (GM == 1) {
+          int ko, kk;
+          gather_k(ga, (gw.kb0 + gkb) * BK + lane, ko, kk);
+          const uint32_t row = st2 + C::kOffA + r * 128;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            gather_cp(ga, zs, gpb, gy0, gx0, __shfl_sync(0xffffffffu, ko, j), __shfl_sync(0xffffffffu, kk, j),
+                      row + ((((j >> 2) ^ (r & 7))) << 4) + ((j & 3) << 2));
+        } else {
+          int pb2, y02, x02;
+          gather_pix(ga, (gw.kb0 + gkb) * BK + lane, pb2, y02, x02);
+          const uint32_t col = (lane & 3) << 2;
+#pragma unroll
+          for (int j = 0; j < C::kRowsB / 4; ++j) {
+            const int i = warp - 2 + 4 * j;
+            const int ko = __shfl_sync(0xffffffffu, gk[j >> 5], j & 31);
+            const int kk = __shfl_sync(0xffffffffu, gkk[j >> 5], j & 31);
+            gather_cp(ga, zs, pb2, y02, x02, ko, kk,
+                      st2 + C::kOffB + i * 128 + ((((lane >> 2) ^ (i & 7))) << 4) + col);
+          }
+        }
+        cp_async_arrive(full0 + 8 * s2);
+        ++gg;
+        if (++gkb >= gw.nkb) {
+          gkb = 0;
+          gu += ustep;
+          if (gu < nunits) {
+            gw = unit_of(gu, ep, ntn, ntm, nkb_all, BN, BMU);
+            unit_rows();
+          }
+        }
+      };
+      if (GM == 1 || GM == 2)
+        for (int d = 0; d < kAhead; ++d) gather_next();
       for (int u = ubase; u < nunits; u += ustep) {
         const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
-        const float* zs = GM ? ga.src + (int64_t)w.z * ga.sb : nullptr;
-        int pb = 0, py0 = 0, px0 = 0;  // GM = 1: this thread's row (a pixel of the M grid)
-        if (GM == 1) gather_pix(ga, w.m0 + arow + r, pb, py0, px0);
-        if (GM == 2) {  // (koff, kh|kw) of this CTA's B rows, once per unit
-          named_bar_sync(3, 128);  // the previous unit's last k-block no longer reads the table
-          for (int i = et; i < C::kRowsB; i += 128) {
-            int ko, kw;
-            gather_k(ga, w.n0 + brow + i < ep.n ? w.n0 + brow + i : ga.kdim, ko, kw);
-            btab[i] = make_int2(ko, kw);
-          }
-          named_bar_sync(3, 128);
+        int hb = 0, hy0 = 0, hx0 = 0;  // GM = 3: this thread's pixel inside the unit's halo
+        if (GM == 3) {
+          int r_lo, r_hi, pb_unused;
+          halo_rows(ga, w.m0 + arow, r_lo, r_hi);
+          gather_pix(ga, w.m0 + arow + r, pb_unused, hy0, hx0);
+          const int m = w.m0 + arow + r, hw = ga.MH * ga.MW;
+          hb = ((r_lo * ga.SW) & 3) + ((m / hw) * ga.SH + hy0 - r_lo) * ga.SW + hx0;
         }
         for (int kb = 0; kb < w.nkb; ++kb, ++g) {
           const int s = g % C::kStages;
+          if (GM == 1 || GM == 2) gather_next();  // k-block g + kAhead
           mbar_wait(full0 + 8 * s, (g / C::kStages) & 1);
           if (warp == 2 && lane == 0) TRACE(3, g);
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           const uint32_t sa = st + C::kOffA;
           uint32_t hi[32], lo[32];
-          if (GM == 1) {  // A row r gathered from the activations (implicit im2col)
+          if (GM == 3) {  // A row r read from the halo: lane-consecutive pixels -> consecutive words
+            const int k0 = (w.kb0 + kb) * BK, c_lo = k0 / (ga.KH * ga.KW);
             int ko, kk;
-            gather_k(ga, (w.kb0 + kb) * BK + lane, ko, kk);
-            float xv[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              xv[j] = gather_ld(ga, zs, pb, py0, px0, __shfl_sync(0xffffffffu, ko, j),
-                                __shfl_sync(0xffffffffu, kk, j));
+            gather_k(ga, k0 + lane, ko, kk);
+            if (k0 + lane < ga.kdim) {  // channel-local offset inside the halo
+              const int ch = (k0 + lane) / (ga.KH * ga.KW);
+              ko = (ch - c_lo) * ga.hpitch + ga.sgn * ((kk & 0xffff) * ga.SW + (kk >> 16));
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float h = tf32_hi(xv[j]);
+              const int koj = __shfl_sync(0xffffffffu, ko, j), kkj = __shfl_sync(0xffffffffu, kk, j);
+              const int y = hy0 + ga.sgn * (kkj & 0xffff), x = hx0 + ga.sgn * (kkj >> 16);
+              float v = 0.f;
+              if ((unsigned)y < (unsigned)ga.SH && (unsigned)x < (unsigned)ga.SW)
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(sa + 4 * (hb + koj)));
+              const float h = tf32_hi(v);
               hi[j] = __float_as_uint(h);
-              lo[j] = __float_as_uint(__fsub_rn(xv[j], h));
+              lo[j] = __float_as_uint(__fsub_rn(v, h));
             }
-          } else if (!AMN) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
+          } else if (!AMN || GM == 1) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const float4 x = lds4(sa + r * 128 + ((c ^ (r & 7)) << 4));
@@ -787,21 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // every split thread has read its A row: B lo may overwrite the tile
           named_bar_sync(3, 128);
 #ifndef ESGD_X_NOSPLITB
-          if (GM == 2) {
-            // B rows gathered from the activations: lane = pixel (coalesced),
-            // raw value (= B_hi to the tensor core) and lo into the SW128 rows
-            int pb2, y02, x02;
-            gather_pix(ga, (w.kb0 + kb) * BK + lane, pb2, y02, x02);
-            const uint32_t col = ((lane & 3) << 2);
-            for (int i = warp - 2; i < C::kRowsB; i += 4) {
-              const int2 t = btab[i];
-              const float v = gather_ld(ga, zs, pb2, y02, x02, t.x, t.y);
-              const uint32_t off = i * 128 + ((((lane >> 2) ^ (i & 7))) << 4) + col;
-              const float h = tf32_hi(v);
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + C::kOffB + off), "f"(v) : "memory");
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + C::kOffBLo + off), "f"(__fsub_rn(v, h)) : "memory");
-            }
-          } else {
+          {
             split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
           }
 #endif
@@ -1098,7 +1197,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
   int rc = ESGD_OK;
-  if (GM != 1) {  // (a gathered operand has no tensor map)
+  if (GM == 0 || GM == 2) {  // (a gathered operand has no tensor map)
     rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN, /*atom32=*/!SPLIT);
     if (rc) return rc;
   }
@@ -1178,7 +1277,8 @@ template <int BN>
 int launch_split(const Plan& p, cudaStream_t st) {
   return p.pair ? launch_major<BN, true, true>(p, st) : launch_major<BN, true, false>(p, st);
 }
-// implicit-GEMM convolutions: GM = 1 gathers A (K-major B), GM = 2 gathers B (K-major A)
+// implicit-GEMM convolutions: GM = 1 gathers A (K-major B), GM = 2 gathers B (K-major A),
+// GM = 3 reads A from a per-k-block halo of source rows
 template <int BN, int GM>
 int launch_gather(const Plan& p, cudaStream_t st, const Gather& ga) {
   return p.pair ? launch<BN, true, false, false, true, GM>(p, st, ga) : launch<BN, true, false, false, false, GM>(p, st, ga);
@@ -1245,8 +1345,11 @@ extern "C" int esgd_tc_conv_f32(const esgd_tc_gemm_desc* d, const esgd_conv_gath
   ESGD_REQUIRE(cg->src && cg->kh >= 1 && cg->kw >= 1 && cg->channels >= 1 && cg->stride >= 1 &&
                    (cg->sgn == 1 || cg->sgn == -1) && cg->src_h >= 1 && cg->src_w >= 1 && cg->grid_h >= 1 &&
                    cg->grid_w >= 1 && cg->npix >= 1 && cg->npix % (cg->grid_h * cg->grid_w) == 0 &&
-                   (int64_t)cg->plane >= (int64_t)(cg->npix / (cg->grid_h * cg->grid_w)) * cg->src_h * cg->src_w,
+                   cg->img_stride >= 0,
                ESGD_ERR_INPUT, "tc_conv: bad gather geometry");
+  if ((cg->img_stride == 0 || cg->img_stride == cg->src_h * cg->src_w) && cg->channels > 1)  // CNHW planes
+    ESGD_REQUIRE((int64_t)cg->plane >= (int64_t)(cg->npix / (cg->grid_h * cg->grid_w)) * cg->src_h * cg->src_w,
+                 ESGD_ERR_INPUT, "tc_conv: channel plane shorter than its images");
   ESGD_REQUIRE((int64_t)cg->plane * cg->channels < (int64_t(1) << 31) && kdim < (int64_t(1) << 30),
                ESGD_ERR_UNSUPPORTED, "tc_conv: source tensor too large for 32-bit offsets");
   if (side == 1) {
@@ -1265,14 +1368,48 @@ extern "C" int esgd_tc_conv_f32(const esgd_tc_gemm_desc* d, const esgd_conv_gath
   ESGD_REQUIRE(d->c, ESGD_ERR_INPUT, "tc_conv: null output");
   ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
                "tc_conv: batch strides must be multiples of 4");
-  tc::Gather ga{cg->src, cg->src_sb, cg->plane, cg->src_h, cg->src_w, cg->grid_h, cg->grid_w, cg->stride,
-                cg->yoff, cg->xoff, cg->sgn, cg->kh, cg->kw, cg->npix, (int)kdim};
+  const int nstride = cg->img_stride ? cg->img_stride : cg->src_h * cg->src_w;
+  // a single-channel source: its "plane" (the halo copies' bound) is all its images
+  const int plane = (cg->channels == 1 && nstride == cg->src_h * cg->src_w)
+                        ? ((cg->npix / (cg->grid_h * cg->grid_w)) * cg->src_h * cg->src_w + 3) & ~3
+                        : cg->plane;
+  tc::Gather ga{cg->src, cg->src_sb, plane, nstride, cg->src_h, cg->src_w, cg->grid_h, cg->grid_w,
+                cg->stride, cg->yoff, cg->xoff, cg->sgn, cg->kh, cg->kw, cg->npix, (int)kdim, 0};
+  // side 1: the source rows of each 128-pixel tile staged once per k-block as
+  // a halo (one bulk copy per channel the k-block touches) when they fit in
+  // the A tile's 16 KB — the split warps then read A from shared memory;
+  // otherwise (AlexNet conv1's 224-wide rows) per-element cp.async gathers
+  bool halo = false;
+  if (side == 1 && nstride == cg->src_h * cg->src_w && !getenv("ESGD_NO_HALO")) {  // (CNHW planes)
+    const int hw = cg->grid_h * cg->grid_w, reach = cg->sgn * (cg->kh - 1);
+    const int nimg = cg->npix / hw;
+    int64_t lmax = 0;
+    for (int m0 = 0; m0 < cg->npix; m0 += tc::BM) {
+      const int last = std::min(m0 + tc::BM, cg->npix) - 1;
+      const int n0 = m0 / hw, y0 = ((m0 - n0 * hw) / cg->grid_w) * cg->stride + cg->yoff;
+      const int n1 = last / hw, y1 = ((last - n1 * hw) / cg->grid_w) * cg->stride + cg->yoff;
+      const int r_lo = std::max(0, n0 * cg->src_h + y0 + std::min(0, reach));
+      const int r_hi = std::min(nimg * cg->src_h - 1, n1 * cg->src_h + y1 + std::max(0, reach));
+      const int64_t e0 = (int64_t)r_lo * cg->src_w;
+      const int64_t len = (e0 - (e0 & ~int64_t(3)) + (int64_t)(r_hi - r_lo + 1) * cg->src_w + 3) & ~int64_t(3);
+      lmax = std::max(lmax, len);
+    }
+    const int kk = cg->kh * cg->kw;
+    const int hchan = (tc::BK - 1) / kk + 2;
+    ga.hpitch = (int)((lmax + 3) & ~int64_t(3));
+    halo = (int64_t)hchan * ga.hpitch * 4 <= tc::kTileBytesA;
+  }
   const tc::Plan p = tc::make_plan(d, /*allow_swap=*/false);
   const int64_t need = tc::ws_need(p);
   ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
                "tc_conv: split-K workspace too small (need %lld floats, have %lld; size it with "
                "esgd_tc_conv_ws_floats)", (long long)need, (long long)d->ws_floats);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (side == 1 && halo) {
+    if (p.bn == 64) return tc::launch_gather<64, 3>(p, st, ga);
+    if (p.bn == 192) return tc::launch_gather<192, 3>(p, st, ga);
+    return tc::launch_gather<128, 3>(p, st, ga);
+  }
   if (side == 1) {
     if (p.bn == 64) return tc::launch_gather<64, 1>(p, st, ga);
     if (p.bn == 192) return tc::launch_gather<192, 1>(p, st, ga);

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import ACT, GemmDesc, TcGemmDesc, Tensor4, cnhw, nchw
+from ._lib import ACT, ConvGather, GemmDesc, TcGemmDesc, Tensor4, cnhw, nchw
 from .device import round_up
 from .errors import InputError, ShapeError
 from .network import Conv, ConvNetSpec, Dense, ModelSpec, Pool, view_table
@@ -46,6 +46,11 @@ import os
 # (measured on B200: LeNet's <=1e8-MAC GEMMs are faster on the split-K FFMA
 # kernel, every AlexNet contraction (>=5e8 MACs) on tcgen05)
 TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 28)))
+# ESGD_IMPLICIT=1: tensor-core conv layers as implicit GEMMs (esgd_tc_conv_f32:
+# operands gathered from the activations, no im2col / col2im buffers). Off by
+# default: on AlexNet b=128 the gathered-operand GEMMs measured slower than
+# TMA-fed explicit GEMMs + im2col/col2im (profiles/r02_implicit_conv.md)
+IMPLICIT = os.environ.get("ESGD_IMPLICIT", "0") == "1"
 
 
 class _FakeRows:
@@ -89,6 +94,7 @@ class _Layer:
     kp: int = 0                # K rounded up to 4 (padded weight pitch)
     flatten_in: bool = False   # dense whose input is a spatial tensor
     np4: int = 0               # output plane pitch (b*OH*OW rounded up to 4)
+    implicit: bool = False     # conv as implicit GEMMs (esgd_tc_conv_f32)
 
 
 class DeviceNet:
@@ -96,7 +102,7 @@ class DeviceNet:
     fixed batch ``b``."""
 
     def __init__(self, spec, b: int, nrep: int, device: torch.device, ldw: int | None = None,
-                 use_tc: bool = True, precision: int = 3):
+                 use_tc: bool = True, precision: int = 3, implicit: bool | None = None):
         if isinstance(spec, ModelSpec):
             spec = spec.as_layers()
         if not isinstance(spec, ConvNetSpec):
@@ -107,6 +113,7 @@ class DeviceNet:
         self.ldw = ldw if ldw is not None else round_up(self.n, 64)
         self.use_tc = use_tc
         self.precision = precision
+        self.implicit = (IMPLICIT if implicit is None else implicit) and use_tc and precision == 3
         views = {v.name: v for v in view_table(spec)}
         self.layers: list[_Layer] = []
         prev_spatial = False
@@ -151,19 +158,25 @@ class DeviceNet:
         self.outs, self.cols, self.amax, self.flat, self.pre = [], [], [], [], []
         max_act = b * self.d_in
         max_cols = 1
-        for L in self.layers:
+        first_param = next(j for j, L in enumerate(self.layers) if L.kind != "pool")
+        for j, L in enumerate(self.layers):
             if L.kind in ("conv", "pool"):
                 L.np4 = round_up(b * L.hout * L.wout, 4)
                 size = L.cout * L.np4
             else:
                 size = b * L.cout
+            if L.kind == "conv":
+                # implicit only where the tensor cores take the layer, and the data
+                # gradient (when needed) is a stride-1 transposed window
+                L.implicit = (self.implicit and L.np4 * L.k * L.cout >= TC_MIN_FLOPS and
+                              (L.lay.stride == 1 or j <= first_param))
             max_act = max(max_act, size, b * L.cin * L.hin * L.win)
             if L.flatten_in or L.kind != "dense":
                 prev = self.layers[self.layers.index(L) - 1] if self.layers.index(L) > 0 else None
                 if prev is not None and prev.kind != "dense":
                     max_act = max(max_act, prev.cout * prev.np4)
             self.outs.append(self._t(size))
-            self.cols.append(self._t(L.k * L.np4) if L.kind == "conv" else None)
+            self.cols.append(self._t(L.k * L.np4) if (L.kind == "conv" and not L.implicit) else None)
             self.amax.append(self._t(b * L.cout * L.hout * L.wout, torch.int32) if L.kind == "pool" else None)
             self.flat.append(self._t(b * L.cin * L.hin * L.win) if (L.kind == "dense" and L.flatten_in) else None)
             self.pre.append(self._t(size) if (L.kind == "dense" and L.act in (2, 3)) else None)
@@ -171,7 +184,11 @@ class DeviceNet:
                 max_cols = max(max_cols, L.cout)
         self.d_a = self._t(max_act)
         self.d_b = self._t(max_act)
-        self.dcol = self._t(max((L.k * L.np4 for L in self.layers if L.kind == "conv"), default=4))
+        self.dcol = self._t(max((L.k * L.np4 for L in self.layers if L.kind == "conv" and not L.implicit),
+                                default=4))
+        # implicit data gradient: W permuted to [Cin][Cout*k*k] per round (K-major B)
+        self.wd = [self._t(L.cin * round_up(L.cout * L.lay.k * L.lay.k, 4)) if (L.kind == "conv" and L.implicit)
+                   else None for L in self.layers]
         self.scratch = torch.zeros(256 * max_cols * self.nrep + 64, dtype=torch.float32, device=self.device)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=self.device)
         # split-K partials of the GEMMs (weight gradients reduce over b*OH*OW),
@@ -186,7 +203,7 @@ class DeviceNet:
         # for dense wgrad; refreshed every round (they depend on W / delta)
         self.wt, self.dT = [], []
         for L in self.layers:
-            big = self.use_tc and L.kind == "conv" and L.np4 * L.k * L.cout >= TC_MIN_FLOPS
+            big = self.use_tc and L.kind == "conv" and L.np4 * L.k * L.cout >= TC_MIN_FLOPS and not L.implicit
             self.wt.append(self._t(L.k * round_up(L.cout, 4)) if big else None)
             fan_in = L.cin * L.hin * L.win
             big = self.use_tc and L.kind == "dense" and b * fan_in * L.cout >= TC_MIN_FLOPS and fan_in >= 128
@@ -264,6 +281,29 @@ class DeviceNet:
             if self.record is not None:
                 self.record.append(("ffma", d, 2.0 * m * n * k * nb))
 
+    def _conv(self, stream, side, m, n, k, a, lda, a_sb, bm, ldb, b_sb, c, c_sm, c_sn, c_sb, src, src_sb, sd,
+              grid_h, grid_w, stride, off, sgn, kwin, chans, bias=None, bias_sb=0, mask=None, mask_sm=0,
+              mask_sn=0, mask_sb=0, act=0):
+        """Implicit-GEMM convolution (esgd_tc_conv_f32): side 1 gathers A (rows =
+        pixels of the grid_h x grid_w grid), side 2 gathers B (rows = (ch, kh,
+        kw)) from the activation tensor `src` described by Tensor4 `sd`."""
+        ws = self.tc_ws
+        d = TcGemmDesc(m, n, k, self.nrep, a, lda, a_sb, bm, ldb, b_sb, c, c_sm, c_sn, c_sb,
+                       bias, bias_sb, mask, mask_sm, mask_sn, mask_sb, act, 0, 3, 0, 0,
+                       ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0)
+        npix = (m if side == 1 else k)
+        g = ConvGather(src, src_sb, sd.sc, sd.sn, sd.h, sd.w, grid_h, grid_w, stride, off, off, sgn,
+                       kwin, kwin, npix, chans)
+        if self._dry is not None:
+            need = C.c_int64(0)
+            _lib.check(_lib.load().esgd_tc_conv_ws_floats(C.byref(d), C.byref(need)), "tc_conv_ws")
+            self._dry["tc"] = max(self._dry["tc"], need.value)
+            return
+        _lib.check(_lib.load().esgd_tc_conv_f32(C.byref(d), C.byref(g), side, stream), "tc_conv")
+        self.tc_calls += 1
+        if self.record is not None:
+            self.record.append(("tcconv", d, 2.0 * m * n * k * self.nrep, g, side))
+
     # ---- passes ----------------------------------------------------------------
     def forward(self, W: torch.Tensor, stream: int, x: torch.Tensor | None = None) -> torch.Tensor:
         """Forward of all replicas on self.x (or ``x``, same shape); returns
@@ -277,7 +317,20 @@ class DeviceNet:
         for i, L in enumerate(self.layers):
             out = self.outs[i]
             o, o_sb = out.data_ptr(), out.stride(0)
-            if L.kind == "conv":
+            if L.kind == "conv" and L.implicit:
+                lay = L.lay
+                w_ptr, w_pitch, w_sb = wp + 4 * L.w_off, L.k, ldw
+                if self.wpad[i] is not None:
+                    pw = self.wpad[i]
+                    _lib.check(lib.esgd_copy4_f32(pw.data_ptr(), Tensor4(1, L.cout, 1, L.k, 0, L.kp, 0, 1),
+                                                  pw.stride(0), w_ptr, Tensor4(1, L.cout, 1, L.k, 0, L.k, 0, 1),
+                                                  ldw, nb, stream), "pad_weights")
+                    w_ptr, w_pitch, w_sb = pw.data_ptr(), L.kp, pw.stride(0)
+                # out[co][pix] = act(sum_k col[pix][k] W[co][k] + b[co]), col gathered from the input
+                self._conv(stream, 1, b * L.hout * L.wout, L.cout, L.k, None, 0, 0, w_ptr, w_pitch, w_sb,
+                           o, 1, L.np4, o_sb, cur, cur_sb, cur_d, L.hout, L.wout, lay.stride, -lay.pad, 1, lay.k,
+                           L.cin, bias=wp + 4 * L.b_off, bias_sb=ldw, act=L.act)
+            elif L.kind == "conv":
                 col = self.cols[i]
                 lay = L.lay
                 npix = b * L.hout * L.wout
@@ -404,6 +457,33 @@ class DeviceNet:
                 _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd, d_sb,
                                                     self.amax[i].data_ptr(), mask, x_sb, lay.k, lay.stride,
                                                     lay.pad, nb, stream), "maxpool_bwd")
+                dcur = dnext
+            elif L.implicit:  # conv as implicit GEMMs; delta is CNHW [Cout][np4]
+                lay = L.lay
+                npix = b * L.hout * L.wout
+                # dW[co][k] = sum_pix delta[co][pix] col[pix][k], col gathered from the input
+                self._conv(stream, 2, L.cout, L.k, npix, dcur.data_ptr(), L.np4, d_sb, None, 0, 0,
+                           gp + 4 * L.w_off, L.k, 1, ldg, xin, x_sb, xd, L.hout, L.wout, lay.stride, -lay.pad, 1,
+                           lay.k, L.cin)
+                _lib.check(lib.esgd_rowsum_f32(gp + 4 * L.b_off, ldg, dcur.data_ptr(), L.np4, d_sb, L.cout, npix,
+                                               nb, self.scratch.data_ptr(), stream), "rowsum")
+                if not need_dx:
+                    continue
+                # dx[ci][pix] = sum_{co,kh,kw} W[co][ci][kh][kw] delta[co][pix+pad-k] (stride 1), relu
+                # mask of the producer in the epilogue; B = W permuted to [ci][co*k*k]
+                kk = lay.k * lay.k
+                wd, pitch = self.wd[i], round_up(L.cout * kk, 4)
+                _lib.check(lib.esgd_copy4_f32(wd.data_ptr(), Tensor4(1, L.cout, L.cin, kk, 0, kk, pitch, 1),
+                                              wd.stride(0), wp + 4 * L.w_off,
+                                              Tensor4(1, L.cout, L.cin, kk, 0, L.cin * kk, kk, 1), ldw, nb, stream),
+                           "permute_weights")
+                dnext = self._other(dcur)
+                mask = xin if pact == 1 else None
+                yd = self._out_desc(i)
+                self._conv(stream, 1, b * L.hin * L.win, L.cin, L.cout * kk, None, 0, 0, wd.data_ptr(), pitch,
+                           wd.stride(0), dnext.data_ptr(), 1, xd.sc, dnext.stride(0), dcur.data_ptr(), d_sb, yd,
+                           L.hin, L.win, 1, lay.pad, -1, lay.k, L.cout,
+                           mask=mask, mask_sm=1, mask_sn=xd.sc, mask_sb=x_sb)
                 dcur = dnext
             else:  # conv: delta is CNHW [Cout][np4]
                 lay = L.lay

@@ -72,7 +72,7 @@ def test_conv_forward_wgrad_dgrad_vs_fp64(n, cin, h, cout, k, s, p, nrep):
     d = _lib.TcGemmDesc(npo, cout, K, nrep, None, 0, 0, Wd.data_ptr(), kp, Wd.stride(0),
                         out.data_ptr(), 1, oplane, out.stride(0), bd.data_ptr(), bd.stride(0),
                         None, 0, 0, 0, 1, 0, 3, 0, 0, None, 0)
-    g = _lib.ConvGather(Xd.data_ptr(), Xd.stride(0), xplane, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
+    g = _lib.ConvGather(Xd.data_ptr(), Xd.stride(0), xplane, 0, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
     run_conv(d, g, 1)
     cols = []
     for z in range(nrep):
@@ -86,7 +86,7 @@ def test_conv_forward_wgrad_dgrad_vs_fp64(n, cin, h, cout, k, s, p, nrep):
     dW = torch.zeros((nrep, cout * K), device="cuda")
     d = _lib.TcGemmDesc(cout, K, npo, nrep, Dd.data_ptr(), oplane, Dd.stride(0), None, 0, 0,
                         dW.data_ptr(), K, 1, dW.stride(0), None, 0, None, 0, 0, 0, 0, 0, 3, 0, 0, None, 0)
-    g = _lib.ConvGather(Xd.data_ptr(), Xd.stride(0), xplane, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
+    g = _lib.ConvGather(Xd.data_ptr(), Xd.stride(0), xplane, 0, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
     run_conv(d, g, 2)
     for z in range(nrep):
         dz = D[z].astype(np.float64).transpose(1, 0, 2, 3).reshape(cout, -1)   # (cout, npix) CNHW order
@@ -105,7 +105,7 @@ def test_conv_forward_wgrad_dgrad_vs_fp64(n, cin, h, cout, k, s, p, nrep):
     dx = torch.zeros((nrep, cin * xplane), device="cuda")
     d = _lib.TcGemmDesc(npi, cin, kd, nrep, None, 0, 0, Wpd.data_ptr(), kdp, Wpd.stride(0),
                         dx.data_ptr(), 1, xplane, dx.stride(0), None, 0, None, 0, 0, 0, 0, 0, 3, 0, 0, None, 0)
-    g = _lib.ConvGather(Dd.data_ptr(), Dd.stride(0), oplane, oh, oh, h, h, 1, p, p, -1, k, k, npi, cout)
+    g = _lib.ConvGather(Dd.data_ptr(), Dd.stride(0), oplane, 0, oh, oh, h, h, 1, p, p, -1, k, k, npi, cout)
     run_conv(d, g, 1)
     for z in range(nrep):
         dz = D[z].astype(np.float64).transpose(0, 2, 3, 1).reshape(-1, cout)   # (npix NHW, cout)
@@ -119,6 +119,6 @@ def test_conv_forward_wgrad_dgrad_vs_fp64(n, cin, h, cout, k, s, p, nrep):
 def test_conv_rejects_bad_geometry():
     d = _lib.TcGemmDesc(10, 4, 9, 1, None, 0, 0, None, 0, 0, None, 1, 12, 0, None, 0, None, 0, 0, 0, 0, 0, 3,
                         0, 0, None, 0)
-    g = _lib.ConvGather(None, 0, 16, 4, 4, 4, 4, 1, 0, 0, 1, 3, 3, 16, 1)
+    g = _lib.ConvGather(None, 0, 16, 0, 4, 4, 4, 4, 1, 0, 0, 1, 3, 3, 16, 1)
     rc = _lib.load().esgd_tc_conv_f32(C.byref(d), C.byref(g), 1, None)
     assert rc != 0

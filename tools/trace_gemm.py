@@ -22,9 +22,15 @@ from paper_1708_02983_b200 import _lib  # noqa: E402
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "conv2.fwd"
-    shape = next(s for s in bench_gemm.SHAPES if s[0] == name)
     torch.cuda.set_device(0)
-    bench_gemm.run(*shape, 3, reps=1)
+    if name.startswith("implicit:"):  # implicit-GEMM conv layer[:pass], e.g. implicit:conv4:fwd
+        import bench_conv_gemm
+        parts = name.split(":")
+        sys.argv = [sys.argv[0], "--only", parts[1]] + (["--pass", parts[2]] if len(parts) > 2 else [])
+        bench_conv_gemm.main()  # the last launch is traced
+    else:
+        shape = next(s for s in bench_gemm.SHAPES if s[0] == name)
+        bench_gemm.run(*shape, int(sys.argv[2]) if len(sys.argv) > 2 else 3, reps=1)
     lib = _lib.load()
     lib.esgd_trace_copy.restype = C.c_int
     buf = np.zeros((8, 4096), dtype=np.uint64)
