@@ -156,6 +156,55 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+class NvlinkCounter:
+    """NVLink bytes this GPU sent / received over a region, from NVML's
+    per-link data counters (NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES, summed
+    over links; throughput counters in KiB as a fallback). None when the
+    driver exposes neither."""
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            try:
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.fields = None
+            for tx, rx, scale in ((getattr(N, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", None),
+                                   getattr(N, "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", None), 1),
+                                  (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+                                   1024)):
+                if tx is None:
+                    continue
+                self.fields = (tx, rx, scale)
+                v = self.read()
+                if v is not None and (v[0] > 0 or v[1] > 0):
+                    break
+            self.ok = self.fields is not None and self.read() is not None
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        N = self.N
+        tx, rx, scale = self.fields
+        tot = [0, 0]
+        try:
+            for link in range(18):
+                vals = N.nvmlDeviceGetFieldValues(self.h, [(tx, link), (rx, link)])
+                for i, v in enumerate(vals):
+                    if v.nvmlReturn == 0:
+                        tot[i] += int(v.value.ullVal) * scale
+            return tot
+        except Exception:
+            return None
+
+
 def dist_setup(n_gpus: int):
     import torch
     import torch.distributed as dist
@@ -271,6 +320,8 @@ def run_device(args):
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = NvlinkCounter(local) if world > 1 else None
+    nvl0 = nvl.read() if (nvl is not None and nvl.ok) else None
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -285,6 +336,17 @@ def run_device(args):
         if world > 1:
             dist.barrier()
     dt = t0.elapsed_time(t1) / 1e3
+    nvlink = None
+    if nvl0 is not None:
+        nvl1 = nvl.read()
+        if nvl1 is not None:
+            # algorithmic NVLink bytes per GPU per round: NVLS ld_reduce of 1/N of S from the
+            # N-1 peers + multicast of that slice of C to them: 2 (N-1)/N * 4|W| each way
+            # (the same as a ring allreduce's 2 (N-1)/N * 4|W|)
+            alg = 2.0 * (world - 1) / world * 4 * eng.ldw
+            nvlink = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps,
+                      "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
+                      "algorithmic_bytes_per_step_each_way": alg, "source": "nvml per-link counters, rank 0 GPU"}
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -328,8 +390,10 @@ def run_device(args):
     # e2e: run_trainer's host data path (pinned batch H2D + loss D2H every round)
     e2e = run_e2e(args, spec, train, cfg, world) if not args.no_e2e else None
 
-    bd = eng.breakdown(dt)
-    comm_frac = bd["peer_param"] / dt if dt > 0 else 0.0
+    # exposed communication of the graph-replayed round (its twin without the
+    # collective, replayed the same way), measured after the timed rounds
+    comm = eng.exposed_comm(rounds=max(5, min(20, args.steps)))
+    comm_frac = comm["fraction"]
     cpu = cpu_baseline(args, spec, train) if (rank == 0 and world == 1 and not args.no_cpu) else None
     out = {
         "metric": METRIC,
@@ -342,6 +406,8 @@ def run_device(args):
         "roofline": roof,
         "roofline_update": roof_upd,
         "comm_fraction_exposed": round(comm_frac, 4),
+        "comm": {k: (round(v, 7) if isinstance(v, float) else v) for k, v in comm.items()},
+        "nvlink": nvlink,
         "gpu_launches": launches_per_step(eng) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -123,6 +123,7 @@ class SyncEngine:
             self.cabi = CabiComm(dev)
             torch.cuda.synchronize()
         self.graphs = [None, None]
+        self._nocomm = False
         self.nvls_single = nvls_fused_single_kernel()
         self.collective = ("nvls-fused" if self.nvls is not None else
                            ("nccl-cabi" if self.cabi is not None else
@@ -130,7 +131,7 @@ class SyncEngine:
 
     # ---- one round ------------------------------------------------------------
     def _sum(self, stream) -> None:
-        if self.solo:
+        if self.solo or self._nocomm:
             return
         if self.nvls is not None:
             if not self.nvls_single:  # center slice over NVLS, overlapped with the backward
@@ -158,6 +159,12 @@ class SyncEngine:
         self.plan.gradient(self.G, self.W, stream_ptr(stream))
 
     def _update(self, stream) -> None:
+        if self._nocomm:  # timing twin without the cross-GPU part: the local fused update only
+            if self.solo:
+                sync_update_solo_(self.W, self.G, self.C, self.n, self.cfg.hyper, stream)
+            else:
+                sync_update_sum_(self.W, self.G, self.C, self.S, self.S, self.n, self.P, self.cfg.hyper, stream)
+            return
         if self.nvls is not None:
             if self.nvls_single:
                 self.nvls.update(self.W, self.G, self.parity, self.P, self.cfg.hyper, stream)
@@ -210,6 +217,46 @@ class SyncEngine:
         else:
             self.graphs = [g, g]
         self.graph = g
+
+    def exposed_comm(self, rounds: int = 10) -> dict:
+        """Exposed communication of the graph-replayed round, measured: the
+        device time of `rounds` replays of the captured round minus that of a
+        captured twin with the cross-GPU part removed (no allreduce / NVLS
+        center; the local fused update instead), max over ranks. This is the
+        part of the round the collective adds after overlap (the reference's
+        exposed-interval accounting, fabric/engine.py:87-115). Timing only:
+        the twin's rounds leave the ranks' centers inconsistent, so call it
+        after the run's real rounds."""
+        def timed(graph):
+            torch.cuda.synchronize()
+            if self.world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(rounds):
+                graph.replay()
+            b.record()
+            b.synchronize()
+            return _max_over_ranks(a.elapsed_time(b) / 1e3 / rounds, self.device)
+
+        full = self.graphs[self.parity]
+        if full is None:
+            self._capture()
+            full = self.graphs[self.parity]
+        t_full = timed(full)
+        saved = (self.graph, list(self.graphs))
+        self._nocomm = True
+        try:
+            self._capture()
+            twin = self.graphs[self.parity]
+        finally:
+            self._nocomm = False
+            self.graph, self.graphs = saved
+        t_local = timed(twin)
+        exposed = max(0.0, t_full - t_local)
+        return {"round_s": t_full, "round_without_comm_s": t_local, "exposed_s": exposed,
+                "fraction": exposed / t_full if t_full > 0 else 0.0, "rounds": rounds,
+                "collective": self.collective}
 
     def close(self) -> None:
         """Release the captured rounds and the C-ABI communicator (if any).
