@@ -394,6 +394,8 @@ def run_device(args):
     # collective, replayed the same way), measured after the timed rounds
     comm = eng.exposed_comm(rounds=max(5, min(20, args.steps)))
     comm_frac = comm["fraction"]
+    if world > 1:  # the collective alone: achieved NVLink bandwidth (NVML link counters read N/A here)
+        comm["alone"] = eng.time_collective(reps=10)
     cpu = cpu_baseline(args, spec, train) if (rank == 0 and world == 1 and not args.no_cpu) else None
     out = {
         "metric": METRIC,
@@ -406,7 +408,7 @@ def run_device(args):
         "roofline": roof,
         "roofline_update": roof_upd,
         "comm_fraction_exposed": round(comm_frac, 4),
-        "comm": {k: (round(v, 7) if isinstance(v, float) else v) for k, v in comm.items()},
+        "comm": comm,
         "nvlink": nvlink,
         "gpu_launches": launches_per_step(eng) * args.steps,
         "e2e": e2e,

@@ -258,6 +258,33 @@ class SyncEngine:
                 "fraction": exposed / t_full if t_full > 0 else 0.0, "rounds": rounds,
                 "collective": self.collective}
 
+    def time_collective(self, reps: int = 10) -> dict:
+        """The round's cross-GPU part alone (no overlapping work): the NCCL
+        allreduce of the packed local sum S, or the NVLS center kernel
+        (barrier + multimem ld_reduce of this rank's slice of S + center step +
+        multimem store), `reps` eager launches between barriers, max over ranks.
+        Per GPU the NVLS kernel moves (N-1)/N * 4|W| B in (the switch-reduced
+        slice) and the same out (its broadcast), like a ring allreduce's
+        2 (N-1)/N * 4|W|. Timing only (rewrites S / the next center)."""
+        if self.world < 2:
+            return {"s": 0.0, "bytes_per_gpu": 0, "GBps": None}
+        cs = torch.cuda.current_stream()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            if self.nvls is not None:
+                self.nvls.center(self.parity, self.P, self.cfg.hyper, cs)
+            else:
+                self._allreduce(cs)
+        b.record()
+        b.synchronize()
+        t = _max_over_ranks(a.elapsed_time(b) / 1e3 / reps, self.device)
+        nbytes = 2.0 * (self.world - 1) / self.world * 4 * self.ldw
+        return {"s": t, "bytes_per_gpu": nbytes, "GBps": nbytes / t / 1e9 if t > 0 else None,
+                "collective": self.collective}
+
     def close(self) -> None:
         """Release the captured rounds and the C-ABI communicator (if any).
         Idempotent; the engine cannot step afterwards."""
