@@ -369,6 +369,27 @@ int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* 
 int esgd_copy4_f32(float* dst, esgd_tensor4 dd, int64_t d_sb, const float* src, esgd_tensor4 sd,
                    int64_t s_sb, int32_t batch, esgd_stream_t stream);
 
+
+/* ---- device-side parameter server: trainers/asynchronous.py:170-264 ------
+ * Asynchronous EASGD / MEASGD with the master as ONE persistent kernel on the
+ * center's GPU, FCFS by ticket (fabric/engine.py:125-148), no host in the
+ * loop. Per worker cycle on the worker's stream: esgd_async_post (takes a
+ * ticket; W is final), the gradient, esgd_async_wait (until the master has
+ * served this worker's post), then the elastic step against the snapshot.
+ * The master (esgd_async_master_f32) serves `services` tickets in order:
+ * snap_w = C (the pre-update center), C += etarho*(W_w - C)
+ * (updates.py:122-131), over NVLink for workers on other GPUs (peer access:
+ * esgd_enable_peer_access both ways). ctl: esgd_async_ctl_ints(workers)
+ * zeroed int32 on the master GPU; ctl[1] != 0 after a 20 s stall (error).   */
+int esgd_async_ctl_ints(int32_t workers);
+int esgd_enable_peer_access(int32_t device, int32_t peer);
+int esgd_async_master_f32(float* center, int64_t n, const float* const* w_ptrs, float* const* snap_ptrs,
+                          int32_t* ctl, int32_t workers, int64_t services, float etarho, int32_t ctas,
+                          esgd_stream_t stream);
+int esgd_async_post(int32_t* ctl, int32_t workers, int32_t worker, int32_t* my_posts, esgd_stream_t stream);
+int esgd_async_wait(int32_t* ctl, int32_t workers, int32_t worker, const int32_t* my_posts,
+                    esgd_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

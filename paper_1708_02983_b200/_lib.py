@@ -111,6 +111,11 @@ _SIGS = {
     "esgd_gemm_f32": (C.c_int, [C.POINTER(GemmDesc), vp]),
     "esgd_tc_gemm_f32": (C.c_int, [C.POINTER(TcGemmDesc), vp]),
     "esgd_gemm_ws_floats": (C.c_int, [C.POINTER(GemmDesc), C.POINTER(i64)]),
+    "esgd_async_ctl_ints": (C.c_int, [i32]),
+    "esgd_enable_peer_access": (C.c_int, [i32, i32]),
+    "esgd_async_master_f32": (C.c_int, [vp, i64, vp, vp, vp, i32, i64, f32, i32, vp]),
+    "esgd_async_post": (C.c_int, [vp, i32, i32, vp, vp]),
+    "esgd_async_wait": (C.c_int, [vp, i32, i32, vp, vp]),
     "esgd_tc_conv_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
     "esgd_tc_conv_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_tc_gemm_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),

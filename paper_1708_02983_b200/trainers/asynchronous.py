@@ -18,10 +18,19 @@ modes (:190-192) — and every exchange is two kernels on it.
   (momentum) step against that snapshot (:121-142).
 * async-sgd / async-msgd: the worker ships its gradient; the master applies
   (momentum) SGD to the center and the worker adopts the new center.
+
+Device master (default for async-easgd / async-measgd without periodic
+evaluation, ``ESGD_ASYNC_MASTER=device``): no host in the loop at all — the
+master is one persistent kernel on device 0 serving tickets FCFS, each worker
+stream runs post -> gradient -> wait -> elastic step (csrc/async.cu). The
+host only enqueues the workers' cycles in bounded chunks. With periodic
+evaluation (eval_every > 0) or ``ESGD_ASYNC_MASTER=host`` the host-polled
+master above runs instead.
 """
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -56,6 +65,8 @@ def run_asynchronous(cfg: TrainerConfig, problem, cm=None, devices=None) -> RunR
     devs = devices or worker_devices(P)
     slots = [WorkerSlot(w, problem, init, devs[w], cfg.batch_size, cfg.seed,
                         momentum=bool(momentum) and weights_mode, snapshot=weights_mode) for w in range(P)]
+    if weights_mode and cfg.eval_every == 0 and os.environ.get("ESGD_ASYNC_MASTER", "device") == "device":
+        return _run_device_master(cfg, problem, slots, quotas, master_dev, bool(momentum))
     ld = slots[0].ld
     C = torch.zeros(ld, dtype=torch.float32, device=master_dev)
     C[:n] = torch.from_numpy(init).to(master_dev)
@@ -149,6 +160,91 @@ def run_asynchronous(cfg: TrainerConfig, problem, cm=None, devices=None) -> RunR
     torch.cuda.synchronize()
     total = time.perf_counter() - t_start - paused
     info = {"engine": "cuda", "devices": sorted({str(d) for d in devs}), "fcfs": "host-polled completion order"}
+    bd = {c: 0.0 for c in CATEGORIES}
+    return rec.build(cfg.method, total, C[:n].cpu().numpy(), breakdown=bd,
+                     worker_weights=[sl.W[0, :n].cpu().numpy() for sl in slots], engine_info=info)
+
+
+def _run_device_master(cfg: TrainerConfig, problem, slots, quotas, master_dev, momentum: bool) -> RunRecord:
+    """async-easgd / async-measgd with the master as one persistent kernel
+    (esgd_async_master_f32, FCFS by ticket) and every worker cycle enqueued on
+    the worker's own stream: post -> gradient -> wait -> elastic step."""
+    lib = _lib.load()
+    P = len(slots)
+    n, ld = slots[0].n, slots[0].ld
+    h = cfg.hyper
+    eta, mu, er = h.eta32, h.mu32, h.etarho32
+    init = slots[0].W[0, :n].to(master_dev)
+    C = torch.zeros(ld, dtype=torch.float32, device=master_dev)
+    C[:n] = init
+    mi = master_dev.index if master_dev.index is not None else 0
+    for sl in slots:
+        di = sl.device.index if sl.device.index is not None else 0
+        if di != mi:
+            _lib.check(lib.esgd_enable_peer_access(di, mi), "peer access")
+            _lib.check(lib.esgd_enable_peer_access(mi, di), "peer access")
+    ctl = torch.zeros(lib.esgd_async_ctl_ints(P), dtype=torch.int32, device=master_dev)
+    wptr = torch.tensor([sl.W.data_ptr() for sl in slots], dtype=torch.int64, device=master_dev)
+    sptr = torch.tensor([sl.snap.data_ptr() for sl in slots], dtype=torch.int64, device=master_dev)
+    posts = [torch.zeros(1, dtype=torch.int32, device=sl.device) for sl in slots]
+    services = int(sum(quotas))
+    master = torch.cuda.Stream(device=master_dev)
+    chunk = int(os.environ.get("ESGD_ASYNC_CHUNK", "32"))
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t_start = time.perf_counter()
+    with torch.cuda.device(master_dev):
+        t0.record(master)
+    _lib.check(lib.esgd_async_master_f32(C.data_ptr(), n, wptr.data_ptr(), sptr.data_ptr(), ctl.data_ptr(), P,
+                                         services, er, int(os.environ.get("ESGD_ASYNC_CTAS", "8")),
+                                         stream_ptr(master)), "async master")
+
+    def cycle(w: int) -> None:
+        sl = slots[w]
+        with torch.cuda.device(sl.device), torch.cuda.stream(sl.stream):
+            _lib.check(lib.esgd_async_post(ctl.data_ptr(), P, w, posts[w].data_ptr(), sl.s), "async post")
+            sl.gradient()
+            _lib.check(lib.esgd_async_wait(ctl.data_ptr(), P, w, posts[w].data_ptr(), sl.s), "async wait")
+            if momentum:
+                _lib.check(lib.esgd_measgd_update_f32(sl.W.data_ptr(), sl.V.data_ptr(), sl.G.data_ptr(),
+                                                      sl.snap.data_ptr(), n, eta, mu, er, sl.s))
+            else:
+                _lib.check(lib.esgd_worker_step_f32(sl.W.data_ptr(), sl.W.data_ptr(), sl.G.data_ptr(),
+                                                    sl.snap.data_ptr(), n, eta, er, sl.s))
+        sl.done += 1
+
+    # every worker's cycles are enqueued round-robin in chunks; a worker never
+    # runs more than two chunks ahead of what has completed, so the host never
+    # blocks on one full stream queue while another worker still needs its post
+    marks: list[list[torch.cuda.Event]] = [[] for _ in range(P)]
+    while any(sl.done < q for sl, q in zip(slots, quotas)):
+        for w, sl in enumerate(slots):
+            if sl.done >= quotas[w]:
+                continue
+            if len(marks[w]) >= 2:
+                marks[w].pop(0).synchronize()
+            for _ in range(min(chunk, quotas[w] - sl.done)):
+                cycle(w)
+            ev = torch.cuda.Event()
+            ev.record(sl.stream)
+            marks[w].append(ev)
+    t1 = torch.cuda.Event(enable_timing=True)
+    for sl in slots:
+        with torch.cuda.device(master_dev):
+            master.wait_stream(sl.stream)
+    with torch.cuda.device(master_dev):
+        t1.record(master)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_start
+    err = int(ctl[1].item())
+    if err:
+        from ..errors import CudaError
+        raise CudaError(f"async device master stalled (code {err})")
+    total = t0.elapsed_time(t1) / 1e3
+    rec = Recorder(problem, 0, cfg.iterations)
+    rec.record(cfg.iterations, total, C[:n])  # the final evaluation (off the clock)
+    info = {"engine": "cuda", "devices": sorted({str(sl.device) for sl in slots}),
+            "fcfs": "device tickets (persistent master kernel)", "wall_s": wall, "services": services}
     bd = {c: 0.0 for c in CATEGORIES}
     return rec.build(cfg.method, total, C[:n].cpu().numpy(), breakdown=bd,
                      worker_weights=[sl.W[0, :n].cpu().numpy() for sl in slots], engine_info=info)
