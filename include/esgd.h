@@ -382,6 +382,9 @@ int esgd_copy4_f32(float* dst, esgd_tensor4 dd, int64_t d_sb, const float* src, 
  * esgd_enable_peer_access both ways). ctl: esgd_async_ctl_ints(workers)
  * zeroed int32 on the master GPU; ctl[1] != 0 after a 20 s stall (error).   */
 int esgd_async_ctl_ints(int32_t workers);
+/* load the protocol's kernels on the current device before the master runs
+ * (a lazy load at first launch can wait on the running master)             */
+int esgd_async_preload(void);
 int esgd_enable_peer_access(int32_t device, int32_t peer);
 int esgd_async_master_f32(float* center, int64_t n, const float* const* w_ptrs, float* const* snap_ptrs,
                           int32_t* ctl, int32_t workers, int64_t services, float etarho, int32_t ctas,

@@ -112,6 +112,7 @@ _SIGS = {
     "esgd_tc_gemm_f32": (C.c_int, [C.POINTER(TcGemmDesc), vp]),
     "esgd_gemm_ws_floats": (C.c_int, [C.POINTER(GemmDesc), C.POINTER(i64)]),
     "esgd_async_ctl_ints": (C.c_int, [i32]),
+    "esgd_async_preload": (C.c_int, []),
     "esgd_enable_peer_access": (C.c_int, [i32, i32]),
     "esgd_async_master_f32": (C.c_int, [vp, i64, vp, vp, vp, i32, i64, f32, i32, vp]),
     "esgd_async_post": (C.c_int, [vp, i32, i32, vp, vp]),

@@ -160,6 +160,18 @@ using namespace esgd;
 
 extern "C" int esgd_async_ctl_ints(int32_t workers) { return 16 + 4 * workers + workers; }
 
+// CUDA loads kernels lazily at their first launch, and a load can wait for
+// running kernels — a spinning master would then wait for a post kernel that
+// waits for its own load. Load the protocol's kernels up front (current device).
+extern "C" int esgd_async_preload(void) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k_async_post);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_async_wait);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, k_async_master);
+  ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "async preload: %s", cudaGetErrorString(e));
+  return ESGD_OK;
+}
+
 extern "C" int esgd_enable_peer_access(int32_t device, int32_t peer) {
   if (device == peer) return ESGD_OK;
   int can = 0;

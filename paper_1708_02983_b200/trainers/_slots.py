@@ -31,6 +31,7 @@ class WorkerSlot:
             self.plan.set_streams([stream_seed(seed, wid)])
         self.done = 0
         self.graph = None
+        self.no_graph = False
         self.calls = 0
 
     @property
@@ -44,7 +45,7 @@ class WorkerSlot:
         the next batches): a replay is one host call instead of ~30 launches,
         which is what bounds the asynchronous schedules' throughput."""
         with torch.cuda.device(self.device):
-            if self.graph is None and self.calls >= 1:
+            if self.graph is None and self.calls >= 1 and not self.no_graph:
                 self._capture()
             if self.graph is not None:
                 with torch.cuda.stream(self.stream):
@@ -52,6 +53,15 @@ class WorkerSlot:
             else:
                 self.plan.gradient(self.G, self.W, self.s)
             self.calls += 1
+
+    def prepare_graph(self) -> None:
+        """Capture the gradient graph now (no execution). Capturing
+        synchronises the device, so it must happen before a persistent kernel
+        that depends on this worker's progress (the async device master) runs."""
+        if self.graph is None:
+            with torch.cuda.device(self.device):
+                self._capture()
+            self.calls = max(self.calls, 1)
 
     def _capture(self) -> None:
         rng = getattr(self.plan, "rng", None)
@@ -66,6 +76,7 @@ class WorkerSlot:
             warnings.warn(f"worker {self.wid}: CUDA graph capture failed ({exc}); running eagerly",
                           RuntimeWarning, stacklevel=2)
             torch.cuda.synchronize(self.device)
+            self.no_graph = True
             return
         self.stream.wait_stream(side)
         if before is not None:  # capture does not execute; keep the RNG where it was

@@ -66,7 +66,10 @@ def run_asynchronous(cfg: TrainerConfig, problem, cm=None, devices=None) -> RunR
     slots = [WorkerSlot(w, problem, init, devs[w], cfg.batch_size, cfg.seed,
                         momentum=bool(momentum) and weights_mode, snapshot=weights_mode) for w in range(P)]
     if weights_mode and cfg.eval_every == 0 and os.environ.get("ESGD_ASYNC_MASTER", "device") == "device":
-        return _run_device_master(cfg, problem, slots, quotas, master_dev, bool(momentum))
+        for sl in slots:
+            sl.prepare_graph()
+        if all(sl.graph is not None for sl in slots):  # (eager gradients could lazily load kernels mid-run)
+            return _run_device_master(cfg, problem, slots, quotas, master_dev, bool(momentum))
     ld = slots[0].ld
     C = torch.zeros(ld, dtype=torch.float32, device=master_dev)
     C[:n] = torch.from_numpy(init).to(master_dev)
@@ -190,6 +193,20 @@ def _run_device_master(cfg: TrainerConfig, problem, slots, quotas, master_dev, m
     services = int(sum(quotas))
     master = torch.cuda.Stream(device=master_dev)
     chunk = int(os.environ.get("ESGD_ASYNC_CHUNK", "32"))
+    for sl in slots:  # graph capture synchronises the device: before the master runs
+        sl.prepare_graph()
+    # every kernel a worker cycle launches must be loaded before the master
+    # spins (lazy loading at a first launch can wait on running kernels)
+    for d in {sl.device for sl in slots} | {master_dev}:
+        with torch.cuda.device(d):
+            _lib.check(lib.esgd_async_preload(), "async preload")
+            z = torch.zeros(4, device=d)
+            if momentum:
+                _lib.check(lib.esgd_measgd_update_f32(z.data_ptr(), z.data_ptr(), z.data_ptr(), z.data_ptr(), 4,
+                                                      eta, mu, er, None))
+            else:
+                _lib.check(lib.esgd_worker_step_f32(z.data_ptr(), z.data_ptr(), z.data_ptr(), z.data_ptr(), 4,
+                                                    eta, er, None))
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t_start = time.perf_counter()
@@ -239,7 +256,11 @@ def _run_device_master(cfg: TrainerConfig, problem, slots, quotas, master_dev, m
     err = int(ctl[1].item())
     if err:
         from ..errors import CudaError
-        raise CudaError(f"async device master stalled (code {err})")
+        c = ctl.cpu().numpy()
+        Q = 2 * P
+        raise CudaError(f"async device master stalled (code {err}): tickets {c[0]}, published "
+                        f"{c[16 + Q:16 + 2 * Q].tolist()}, served {c[16 + 2 * Q:16 + 2 * Q + P].tolist()}, "
+                        f"posts {[int(x.item()) for x in posts]}, done {[sl.done for sl in slots]} of {quotas}")
     total = t0.elapsed_time(t1) / 1e3
     rec = Recorder(problem, 0, cfg.iterations)
     rec.record(cfg.iterations, total, C[:n])  # the final evaluation (off the clock)
