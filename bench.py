@@ -646,6 +646,48 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def run_async(args):
+    """--schedule async-measgd|async-easgd|hogwild-easgd: configs[2] / [3]
+     — the asynchronous schedules in ONE process over
+    the visible GPUs (workers spread round-robin, master on GPU 0: the device
+    master kernel for the elastic async methods). A step = one exchange
+    (one worker cycle); value = exchanges x batch / device time. Under torchrun
+    only rank 0 runs."""
+    import torch
+
+    from paper_1708_02983_b200 import HyperParams, make_config, network, run_trainer
+    from paper_1708_02983_b200.trainers import NetworkProblem
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    model = args.model if args.model != "alexnet" else ("cifar-quick" if "async" in args.schedule else "lenet")
+    wl = WORKLOADS[model]
+    spec = network.MODELS[model](seed=0)
+    train, _ = make_data(model, spec)
+    prob = NetworkProblem(spec, train)
+    b = args.batch or wl["b"]
+    workers = args.workers or (8 if "async" in args.schedule else 16)
+    mom = "measgd" in args.schedule
+    hy = HyperParams(eta=wl["eta"] * (0.1 if mom else 1.0), rho=wl["rho"], mu=0.9)
+    iters = max(args.steps, 1) * workers
+    run_trainer(make_config(args.schedule, workers=workers, iterations=max(args.warmup, 3) * workers,
+                            batch_size=b, hyper=hy, seed=3), prob)  # warm-up: allocation, graphs, kernels
+    rec = run_trainer(make_config(args.schedule, workers=workers, iterations=iters, batch_size=b, hyper=hy,
+                                  seed=3), prob)
+    gpus = torch.cuda.device_count()
+    out = {"metric": f"{args.schedule} samples/s ({workers} workers, {model})", "value": round(iters * b / rec.total_seconds, 1),
+           "unit": "samples/s", "n_gpus": gpus, "steps": iters, "warmup": max(args.warmup, 3) * workers,
+           "ms_per_step": round(rec.total_seconds / iters * 1e3, 5), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (gen_synthetic blobs, HBM-resident)",
+           "config": {"workload": f"configs[{2 if 'async' in args.schedule else 3}]: {args.schedule}, {model}, "
+                                  f"{workers} workers over {gpus} GPU(s), b={b}", "model": model,
+                      "workers": workers, "per_worker_batch": b},
+           "exchanges_per_s": round(iters / rec.total_seconds, 1),
+           "final_train_loss": rec.train_loss[-1] if rec.train_loss else None,
+           "engine": rec.engine_info}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -656,10 +698,15 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--schedule", default="sync-easgd3",
+                    choices=["sync-easgd3", "async-measgd", "async-easgd", "hogwild-easgd"])
+    ap.add_argument("--workers", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.schedule != "sync-easgd3" and args.impl == "native":
+        run_async(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_device(args)
