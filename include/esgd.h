@@ -56,6 +56,11 @@ int esgd_worker_step_f32(float* w_out, const float* w, const float* g, const flo
  *   c_out = c + etarho*(s - P*c);  c_out may alias c.                      */
 int esgd_center_step_from_sum_f32(float* c_out, const float* c, const float* s, int64_t n,
                                   float etarho, int32_t num_workers, esgd_stream_t stream);
+/* Snapshot form, updates.py:96-110: C' = C + etarho * sum_i (W_i - C) with the
+ * sum in worker order (rows of `snaps`, pitch lds floats) — bitwise the
+ * reference's fp32 arithmetic (the from-sum form differs by rounding).      */
+int esgd_center_step_snapshots_f32(float* c_out, const float* c, const float* snaps, int64_t lds,
+                                   int32_t num_workers, int64_t n, float etarho, esgd_stream_t stream);
 
 /* _sync_round, trainers/synchronous.py:57-64 (fused, in place):
  * for every local replica r < nrep:

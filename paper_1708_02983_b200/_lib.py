@@ -96,6 +96,7 @@ _SIGS = {
     "esgd_worker_step_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, i64, f32, f32, vp]),
     "esgd_sync_update_sum_f32": (C.c_int, [vp, i64, vp, i64, i32, vp, vp, vp, i64, f32, f32, i32, vp]),
     "esgd_measgd_update_f32": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, f32, vp]),
+    "esgd_center_step_snapshots_f32": (C.c_int, [vp, vp, vp, i64, i32, i64, f32, vp]),
     "esgd_sync_update_solo_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),
     "esgd_center_incr_f32": (C.c_int, [vp, vp, vp, i64, f32, vp]),
     "esgd_exchange_update_f32": (C.c_int, [vp, vp, vp, i64, f32, f32, vp]),

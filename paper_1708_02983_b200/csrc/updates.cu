@@ -441,6 +441,30 @@ extern "C" int esgd_sync_update_solo_f32(float* W, const float* G, float* C, int
   return check_launch("esgd_sync_update_solo_f32");
 }
 
+// Snapshot form of the center step (updates.py:96-110) in the reference's
+// exact order: total = sum over workers (fixed order) of (W_i - C), then
+// C + (eta*rho)*total — bitwise the reference's fp32 arithmetic.
+__global__ void __launch_bounds__(256) k_center_snapshots(float* co, const float* c, const float* __restrict__ S,
+                                                          int64_t lds, int P, int64_t n, float er) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float ci = c[i];
+    float t = 0.f;
+    for (int r = 0; r < P; ++r) t = __fadd_rn(t, __fsub_rn(S[r * lds + i], ci));
+    co[i] = __fadd_rn(ci, __fmul_rn(er, t));
+  }
+}
+
+extern "C" int esgd_center_step_snapshots_f32(float* c_out, const float* c, const float* snaps, int64_t lds,
+                                              int32_t num_workers, int64_t n, float etarho, esgd_stream_t stream) {
+  ESGD_REQUIRE(n >= 0 && num_workers >= 1 && (num_workers == 1 || lds >= n), ESGD_ERR_SHAPE,
+               "center_step_snapshots: bad sizes");
+  if (n == 0) return ESGD_OK;
+  ESGD_REQUIRE(c_out && c && snaps, ESGD_ERR_INPUT, "center_step_snapshots: null buffer");
+  k_center_snapshots<<<stride_grid(n, 256), 256, 0, ESGD_STREAM(stream)>>>(c_out, c, snaps, lds, num_workers, n,
+                                                                          etarho);
+  return check_launch("esgd_center_step_snapshots_f32");
+}
+
 extern "C" int esgd_center_step_from_sum_f32(float* c_out, const float* c, const float* s,
                                              int64_t n, float etarho, int32_t num_workers,
                                              esgd_stream_t stream) {

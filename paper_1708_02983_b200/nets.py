@@ -394,15 +394,23 @@ class DeviceNet:
         """G[r] = d(mean CE)/dW[r] on the sampled batch in self.x/self.y."""
         lib = self._L()
         b, nb = self.b, self.nrep
-        wp, ldw = W.data_ptr(), W.stride(0)
-        gp, ldg = G.data_ptr(), G.stride(0)
         logits = self.forward(W, stream)
         # dlogits = (softmax - onehot)/rows, in place over the logits (kernels.py:85-106)
         _lib.check(lib.esgd_softmax_xent_f32(logits.data_ptr(), self.row_loss.data_ptr(), logits.data_ptr(),
                                              self.classes, logits.stride(0), self.y.data_ptr(),
                                              self.y.stride(0), b, self.classes, nb,
                                              self.bad_label.data_ptr(), stream), "softmax_xent")
-        dcur = logits
+        self.backward(G, W, stream)
+
+    def backward(self, G: torch.Tensor, W: torch.Tensor, stream: int) -> None:
+        """G[r] = the packed gradient for the logits' gradient held in the last
+        layer's output buffer (self.outs[-1], (nrep, b*classes)), after a
+        forward of the same W (network.py:176-200)."""
+        lib = self._L()
+        b, nb = self.b, self.nrep
+        wp, ldw = W.data_ptr(), W.stride(0)
+        gp, ldg = G.data_ptr(), G.stride(0)
+        dcur = self.outs[-1]
         first_param = next(j for j, L in enumerate(self.layers) if L.kind != "pool")
         for i in range(len(self.layers) - 1, -1, -1):
             L = self.layers[i]

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import InputError, ShapeError
+from .errors import InputError, ShapeError, StaleCacheError
 from .rng import CounterRng, mix64
 
 ACT_IDS = {"none": 0, "relu": 1, "tanh": 2, "sigmoid": 3}
@@ -232,7 +232,128 @@ def _fans(spec, v: View) -> tuple[int, int]:
     return v.shape[0], v.shape[1]
 
 
-def build_model(spec) -> np.ndarray:
+class PackedWeights:
+    """Contiguous parameter buffer plus the per-layer view table (reference
+    network.py:80-113): views are disjoint, contiguous and cover the buffer
+    exactly; a tensor from :meth:`view` writes through to its slice. The
+    buffer may be a host ndarray or a device tensor of the same layout."""
+
+    def __init__(self, buffer, views: list[View]):
+        covered = 0
+        for v in views:
+            if v.offset != covered:
+                raise ShapeError(f"view {v.name} at offset {v.offset}, expected {covered}")
+            covered += v.size
+        size = buffer.numel() if hasattr(buffer, "numel") else buffer.size
+        if covered != size:
+            raise ShapeError(f"views cover {covered} elements, buffer has {size}")
+        self.buffer = buffer
+        self.views = views
+
+    def view(self, name: str):
+        for v in self.views:
+            if v.name == name:
+                return self.buffer[v.offset:v.offset + v.size].reshape(v.shape)
+        raise KeyError(name)
+
+    def clone(self) -> "PackedWeights":
+        return PackedWeights(self.buffer.clone() if hasattr(self.buffer, "clone") else self.buffer.copy(),
+                             self.views)
+
+    @property
+    def size(self) -> int:
+        return int(self.buffer.numel() if hasattr(self.buffer, "numel") else self.buffer.size)
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.size * (self.buffer.element_size() if hasattr(self.buffer, "element_size")
+                                else self.buffer.itemsize))
+
+
+def packed_weights_for(spec, buffer) -> PackedWeights:
+    """Wrap an existing flat buffer in the view table of ``spec`` (network.py:236-242)."""
+    expected = spec.parameter_count()
+    size = buffer.numel() if hasattr(buffer, "numel") else np.asarray(buffer).size
+    if size != expected:
+        raise ShapeError(f"buffer size {size} != layout size {expected}")
+    if not hasattr(buffer, "numel"):
+        buffer = np.ascontiguousarray(buffer, dtype=spec.dtype)
+    return PackedWeights(buffer, view_table(spec))
+
+
+def build_model(spec) -> PackedWeights:
+    """Xavier-uniform weights, zero biases, deterministic in ``spec.seed``
+    (network.py:128-140; sequential draws across layers), as PackedWeights
+    over a host buffer; ``init_buffer`` returns the flat buffer alone."""
+    return PackedWeights(init_buffer(spec), view_table(spec))
+
+
+@dataclass
+class ForwardCache:
+    """What backward needs from a forward pass (network.py:144-150): here the
+    device executor that ran it, holding the activations in HBM."""
+
+    net: object
+    weights_token: int
+    spec: object
+    W: object
+
+
+def _device_batch(spec, weights: PackedWeights, batch):
+    import torch
+
+    from .device import require_cuda
+    from .nets import DeviceNet
+
+    dev = require_cuda()
+    batch = np.asarray(batch, dtype=np.float32)
+    d_in = spec.input_dim if isinstance(spec, ConvNetSpec) else spec.dims[0]
+    if batch.ndim != 2 or batch.shape[1] != d_in:
+        raise InputError(f"batch shape {batch.shape} does not match input dim {d_in}")
+    n = spec.parameter_count()
+    net = DeviceNet(spec, batch.shape[0], 1, dev)
+    W = torch.zeros((1, net.ldw), dtype=torch.float32, device=dev)
+    buf = weights.buffer
+    W[0, :n] = (buf.to(dev, torch.float32) if hasattr(buf, "numel")
+                else torch.from_numpy(np.ascontiguousarray(buf, dtype=np.float32)).to(dev))
+    net.x[0, :batch.size] = torch.from_numpy(batch.reshape(-1)).to(dev)
+    return net, W
+
+
+def forward(spec, weights: PackedWeights, batch) -> tuple[ForwardCache, np.ndarray]:
+    """Run the network on a (b, input_dim) batch on the device; returns
+    (cache, logits) like the reference (network.py:153-173)."""
+    import torch
+
+    from .device import stream_ptr
+
+    net, W = _device_batch(spec, weights, batch)
+    logits = net.forward(W, stream_ptr())
+    out = logits[0, :net.b * net.classes].reshape(net.b, net.classes).cpu().numpy()
+    torch.cuda.synchronize()
+    return ForwardCache(net, id(weights), spec, W), out.astype(spec.dtype)
+
+
+def backward(spec, weights: PackedWeights, cache: ForwardCache, dlogits) -> np.ndarray:
+    """Gradient of the loss w.r.t. every packed parameter for the logits'
+    gradient ``dlogits`` (network.py:176-200): one buffer of the packed layout."""
+    import torch
+
+    from .device import stream_ptr
+
+    if cache.weights_token != id(weights) or cache.spec is not spec:
+        raise StaleCacheError("cache was produced by a different forward pass")
+    net = cache.net
+    dl = np.asarray(dlogits, dtype=np.float32)
+    if dl.shape != (net.b, net.classes):
+        raise ShapeError(f"dlogits shape {dl.shape} != logits shape {(net.b, net.classes)}")
+    net.outs[-1][0, :dl.size] = torch.from_numpy(dl.reshape(-1)).to(net.device)
+    G = torch.zeros_like(cache.W)
+    net.backward(G, cache.W, stream_ptr())
+    return G[0, :spec.parameter_count()].cpu().numpy().astype(spec.dtype)
+
+
+def init_buffer(spec) -> np.ndarray:
     """Flat host buffer: Xavier-uniform weights, zero biases, deterministic in
     ``spec.seed`` (network.py:128-140; sequential draws across layers)."""
     views = view_table(spec)

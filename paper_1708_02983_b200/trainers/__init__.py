@@ -7,7 +7,7 @@ from ..errors import InputError
 from ..fabric.costmodel import CostModel
 from .config import METHOD_SCHEDULERS, METHODS, TrainerConfig, make_config
 from .problems import NetworkProblem, QuadraticProblem, ZeroGradientProblem
-from .records import RunRecord, weights_digest
+from .records import RunRecord, eval_loss, evaluate, weights_digest
 from .synchronous import SYNC_METHODS, SyncEngine, run_synchronous
 from .hostfeed import HostFedRun
 
@@ -50,6 +50,8 @@ __all__ = [
     "SyncEngine",
     "TrainerConfig",
     "ZeroGradientProblem",
+    "eval_loss",
+    "evaluate",
     "make_config",
     "run_trainer",
     "weights_digest",

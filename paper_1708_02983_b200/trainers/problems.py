@@ -27,7 +27,7 @@ from ..datasets import Dataset
 from ..device import require_cuda, round_up, stream_ptr
 from ..errors import InputError, ShapeError
 from ..nets import DeviceNet
-from ..network import ConvNetSpec, ModelSpec, build_model
+from ..network import ConvNetSpec, ModelSpec, init_buffer
 from ..rng import CounterRng
 from .records import weights_digest
 
@@ -118,7 +118,7 @@ class NetworkProblem:
 
     # -- reference protocol ---------------------------------------------------
     def init_weights(self) -> np.ndarray:
-        return build_model(self.spec)
+        return init_buffer(self.spec)
 
     def gradient(self, weights, rng: CounterRng, batch_size: int) -> np.ndarray:
         """Host-in/host-out gradient at ``weights`` on a batch drawn from

@@ -91,17 +91,21 @@ def easgd_center_step_from_sum(center, weight_sum, num_workers: int, eta: float,
 
 
 def easgd_center_step(center, worker_snapshots, eta: float, rho: float) -> torch.Tensor:
-    """Snapshot form (updates.py:96-110), via the fixed-order device sum and
-    the from-sum rule (equal to 1e-12 in the reference's own test,
-    tests/test_updates.py:101-107)."""
-    from .fabric.collectives import tree_sum
-
+    """Snapshot form (updates.py:96-110): C' = C + (eta*rho) * sum_i (W_i - C),
+    summed in worker order on the device — bitwise the reference's fp32
+    arithmetic (esgd_center_step_snapshots_f32)."""
     snaps = list(worker_snapshots)
     if not snaps:
         raise InputError("easgd_center_step needs at least one worker snapshot")
+    check_f32(center, *snaps)
     for s in snaps:
         same_shape(center, s)
-    return easgd_center_step_from_sum(center, tree_sum(snaps), len(snaps), eta, rho)
+    S = torch.stack([s.reshape(-1) for s in snaps]).contiguous()
+    out = torch.empty_like(center)
+    hy = HyperParams(eta, rho)
+    _lib.call("esgd_center_step_snapshots_f32", ptr(out), ptr(center), ptr(S), S.stride(0), len(snaps),
+              center.numel(), hy.etarho32, stream_ptr())
+    return out
 
 
 def easgd_center_incremental(center, worker, eta: float, rho: float) -> torch.Tensor:

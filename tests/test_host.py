@@ -30,7 +30,7 @@ def test_cnn_layout_and_init_equal_oracle(factory, layers):
     views, total = O.param_views(*layers)
     assert total == spec.parameter_count()
     assert [(v.shape, v.offset) for v in network.view_table(spec)] == [(tuple(s), o) for s, o in views]
-    assert np.array_equal(network.build_model(spec), O.build_model(*layers, 4, np.float32))
+    assert np.array_equal(network.build_model(spec).buffer, O.build_model(*layers, 4, np.float32))
 
 
 def test_mlp_init_equals_reference(golden):
@@ -38,8 +38,8 @@ def test_mlp_init_equals_reference(golden):
     for dt in ("float32", "float64"):
         for act in ("relu", "tanh", "sigmoid"):
             spec = ModelSpec((32, 24, 16, 10), activation=act, seed=1, dtype=np.dtype(dt).type)
-            assert np.array_equal(network.build_model(spec), g[f"{dt}_{act}_init"])
-    assert np.array_equal(network.build_model(ModelSpec((784, 100, 10), seed=0))[:4096], g["big_init_head"])
+            assert np.array_equal(network.build_model(spec).buffer, g[f"{dt}_{act}_init"])
+    assert np.array_equal(network.build_model(ModelSpec((784, 100, 10), seed=0)).buffer[:4096], g["big_init_head"])
 
 
 def test_rng_equals_reference(golden):
