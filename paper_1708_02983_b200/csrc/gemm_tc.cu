@@ -41,7 +41,19 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;                  // 32 fp32 = 128 B = one swizzle atom row
-constexpr int kThreads = 448;           // 14 warps: TMA, MMA, 4 split, 8 drain/epilogue
+constexpr int kThreads = 448;           // 14 warps: TMA, MMA, 4 split, 8 drain/epilogue (BN = 192)
+// split warps per CTA: 4 (one per TMEM lane quadrant). The kernel also runs
+// with 8 (two per quadrant, each half of the 32 K columns; ESGD_SPLIT_WARPS=8
+// at build time, BN <= 128, 96 registers per thread): measured no faster on
+// the AlexNet shapes (conv2 dgrad 0.34 -> 0.37 ms, conv4 dgrad 0.19 -> 0.18 ms)
+// — the split warps are not short of issue slots but of TMEM / smem bandwidth
+#ifndef ESGD_SPLIT_WARPS
+#define ESGD_SPLIT_WARPS 4
+#endif
+__host__ __device__ constexpr int split_warps(int bn, bool split) {
+  return (split && bn <= 128 && ESGD_SPLIT_WARPS == 8) ? 8 : 4;
+}
+__host__ __device__ constexpr int cta_threads(int bn, bool split) { return 32 * (10 + split_warps(bn, split)); }
 constexpr int kDrainWarps = 8;         // two per TMEM lane quadrant, each owning half of the BN columns
 // K-blocks (x32) per TMEM accumulation before promotion into fp32 registers.
 // 4 (128-deep chunks) measured ~8% faster on the AlexNet shapes (the drain's
@@ -254,6 +266,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 // 32 columns of the warp's 32 TMEM lanes, no wait (pair with tmem_wait_ld)
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -452,19 +472,19 @@ __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
 }
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-template <int BYTES>
+template <int BYTES, int NT = 128>
 __device__ __forceinline__ void split_tile(uint32_t raw, uint32_t lo, int tid) {
-  constexpr int kVec = BYTES / 16, kPer = kVec / 128;
+  constexpr int kVec = BYTES / 16, kPer = kVec / NT;
   constexpr int kBatch = kPer <= 8 ? kPer : (kPer % 8 == 0 ? 8 : (kPer % 6 == 0 ? 6 : 4));
-  static_assert(kVec % 128 == 0 && kPer % kBatch == 0, "tile must split evenly over 128 threads");
+  static_assert(kVec % NT == 0 && kPer % kBatch == 0, "tile must split evenly over the threads");
 #pragma unroll
   for (int b0 = 0; b0 < kPer; b0 += kBatch) {
     float4 x[kBatch];
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) x[j] = lds4(raw + 16 * (tid + 128 * (b0 + j)));
+    for (int j = 0; j < kBatch; ++j) x[j] = lds4(raw + 16 * (tid + NT * (b0 + j)));
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      const uint32_t off = 16 * (tid + 128 * (b0 + j));
+      const uint32_t off = 16 * (tid + NT * (b0 + j));
       float4 h, l;
       h.x = tf32_hi(x[j].x); h.y = tf32_hi(x[j].y); h.z = tf32_hi(x[j].z); h.w = tf32_hi(x[j].w);
       l.x = __fsub_rn(x[j].x, h.x); l.y = __fsub_rn(x[j].y, h.y);
@@ -597,11 +617,14 @@ __device__ unsigned long long g_trace[8][kTraceN];
 // barriers (multicast); the peer's split and drain warps arrive on the
 // leader's barriers across the cluster.
 template <int BN, bool SPLIT, bool AMN, bool BMN, bool PAIR, int GM = 0>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(cta_threads(BN, SPLIT), 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               const __grid_constant__ CUtensorMap map_c, Epi ep, Gather ga) {
   using C = Cfg<BN, SPLIT, PAIR>;
   static_assert(GM == 0 || (SPLIT && !AMN && !BMN), "gathered operands: 3xTF32, K-major partner");
+  constexpr int NS = split_warps(BN, SPLIT);   // split warps (warps 2 .. 1+NS)
+  constexpr int KC = 32 / (NS / 4);            // K columns of an A row per split thread
+  constexpr int D0 = 2 + NS;                   // first drain warp
   constexpr int kCtas = PAIR ? 2 : 1;
   constexpr int BMU = BM * kCtas;  // output rows per unit
   extern __shared__ uint8_t smem_raw[];
@@ -628,8 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(full0 + 8 * s, (GM == 1 || GM == 2) ? 1 + 128 : 1);  // + the 128 gathering threads (cp.async arrive)
-      mbar_init(split0 + 8 * s, 4 * kCtas);  // one arrive per split warp (of both CTAs: the leader's is used)
+      mbar_init(full0 + 8 * s, (GM == 1 || GM == 2) ? 1 + 32 * NS : 1);  // + the gathering threads (cp.async arrive)
+      mbar_init(split0 + 8 * s, NS * kCtas);  // one arrive per split warp (of both CTAs: the leader's is used)
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int b = 0; b < C::kAccBufs; ++b) {
@@ -753,12 +776,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < D0) {
     if (SPLIT) {
       // ---- split warps: A row r (= TMEM lane) -> tf32 hi / lo in TMEM;
       //      B tile -> hi in place + lo twin in smem
-      const int et = threadIdx.x - 64;  // 0..127
+      const int et = threadIdx.x - 64;  // 0 .. 32*NS-1
       const int q = warp & 3, r = q * 32 + lane;
+      const int c0 = ((warp - 2) >> 2) * KC;  // this thread's K columns of row r: [c0, c0 + KC)
       uint32_t g = 0;
       // Gathered operand (GM): the split warps also produce it, kAhead
       // k-blocks ahead of the split, with 4-byte cp.async (zero-fill for the
@@ -778,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (GM == 2) {
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
-            const int i = warp - 2 + 4 * (lane + 32 * h2), n = gw.n0 + brow + i;
+            const int i = warp - 2 + NS * (lane + 32 * h2), n = gw.n0 + brow + i;
             gather_k(ga, (i < C::kRowsB && n < ep.n) ? n : ga.kdim, gk[h2], gkk[h2]);
           }
         }
@@ -795,16 +819,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           gather_k(ga, (gw.kb0 + gkb) * BK + lane, ko, kk);
           const uint32_t row = st2 + C::kOffA + r * 128;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int jj = 0; jj < KC; ++jj) {
+            const int j = c0 + jj;
             gather_cp(ga, zs, gpb, gy0, gx0, __shfl_sync(0xffffffffu, ko, j), __shfl_sync(0xffffffffu, kk, j),
                       row + ((((j >> 2) ^ (r & 7))) << 4) + ((j & 3) << 2));
+          }
         } else {
           int pb2, y02, x02;
           gather_pix(ga, (gw.kb0 + gkb) * BK + lane, pb2, y02, x02);
           const uint32_t col = (lane & 3) << 2;
 #pragma unroll
-          for (int j = 0; j < C::kRowsB / 4; ++j) {
-            const int i = warp - 2 + 4 * j;
+          for (int j = 0; j < C::kRowsB / NS; ++j) {
+            const int i = warp - 2 + NS * j;
             const int ko = __shfl_sync(0xffffffffu, gk[j >> 5], j & 31);
             const int kk = __shfl_sync(0xffffffffu, gkk[j >> 5], j & 31);
             gather_cp(ga, zs, pb2, y02, x02, ko, kk,
@@ -841,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (warp == 2 && lane == 0) TRACE(3, g);
           const uint32_t st = smem_u32(smem + s * C::kStageBytes);
           const uint32_t sa = st + C::kOffA;
-          uint32_t hi[32], lo[32];
+          uint32_t hi[KC], lo[KC];
           if (GM == 3) {  // A row r read from the halo: lane-consecutive pixels -> consecutive words
             const int k0 = (w.kb0 + kb) * BK, c_lo = k0 / (ga.KH * ga.KW);
             int ko, kk;
@@ -851,38 +877,41 @@ __global__ void __launch_bounds__(kThreads, 1)
               ko = (ch - c_lo) * ga.hpitch + ga.sgn * ((kk & 0xffff) * ga.SW + (kk >> 16));
             }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int jj = 0; jj < KC; ++jj) {
+              const int j = c0 + jj;
               const int koj = __shfl_sync(0xffffffffu, ko, j), kkj = __shfl_sync(0xffffffffu, kk, j);
               const int y = hy0 + ga.sgn * (kkj & 0xffff), x = hx0 + ga.sgn * (kkj >> 16);
               float v = 0.f;
               if ((unsigned)y < (unsigned)ga.SH && (unsigned)x < (unsigned)ga.SW)
                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(sa + 4 * (hb + koj)));
               const float h = tf32_hi(v);
-              hi[j] = __float_as_uint(h);
-              lo[j] = __float_as_uint(__fsub_rn(v, h));
+              hi[jj] = __float_as_uint(h);
+              lo[jj] = __float_as_uint(__fsub_rn(v, h));
             }
           } else if (!AMN || GM == 1) {  // K-major SW128 tile: row r at r*128 B, 16-B chunk c at (c ^ r%8)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int cc = 0; cc < KC / 4; ++cc) {
+              const int c = c0 / 4 + cc;
               const float4 x = lds4(sa + r * 128 + ((c ^ (r & 7)) << 4));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float h = tf32_hi(xs[e]);
-                hi[4 * c + e] = __float_as_uint(h);
-                lo[4 * c + e] = __float_as_uint(__fsub_rn(xs[e], h));
+                hi[4 * cc + e] = __float_as_uint(h);
+                lo[4 * cc + e] = __float_as_uint(__fsub_rn(xs[e], h));
               }
             }
           } else {  // MN-major SW128 boxes of 32(M) x 32(K): 4 KB per box, 16-B chunk (m%32)/4 ^ k%8
             const uint32_t base = sa + (r >> 5) * 4096 + ((r & 3) << 2);
             const int c4 = (r & 31) >> 2;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
+            for (int kk2 = 0; kk2 < KC; ++kk2) {
+              const int k = c0 + kk2;
               float x;
               asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(base + k * 128 + ((c4 ^ (k & 7)) << 4)));
               const float h = tf32_hi(x);
-              hi[k] = __float_as_uint(h);
-              lo[k] = __float_as_uint(__fsub_rn(x, h));
+              hi[kk2] = __float_as_uint(h);
+              lo[kk2] = __float_as_uint(__fsub_rn(x, h));
             }
           }
           // TMEM A slot g % kASlots: free once the MMAs of k-block g - kASlots
@@ -894,14 +923,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + C::kACol0 + (g % C::kASlots) * 64;
 #ifndef ESGD_X_NOAST
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
+          if constexpr (KC == 32) {
+            tmem_st32(ta, *reinterpret_cast<const uint32_t(*)[32]>(hi));
+            tmem_st32(ta + 32, *reinterpret_cast<const uint32_t(*)[32]>(lo));
+          } else {
+            tmem_st16(ta + c0, hi);
+            tmem_st16(ta + 32 + c0, lo);
+          }
 #endif
           // every split thread has read its A row: B lo may overwrite the tile
-          named_bar_sync(3, 128);
+          named_bar_sync(3, 32 * NS);
 #ifndef ESGD_X_NOSPLITB
           {
-            split_tile<C::kTileBytesB>(st + C::kOffB, st + C::kOffBLo, et);
+            split_tile<C::kTileBytesB, 32 * NS>(st + C::kOffB, st + C::kOffBLo, et);
           }
 #endif
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -925,8 +959,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per lane quadrant halve the registers per thread, so a 32-column slab is
     // loaded per TMEM wait (the drain is bound by the TMEM load latency).
     constexpr int HB = BN / 2;  // columns per drain warp
-    const int q = warp & 3, h = (warp - 6) >> 2;
-    const int issuer = 192 + h * 128;  // lane 0 of warp 6 / warp 10: bulk-store issue
+    const int q = warp & 3, h = (warp - D0) >> 2;
+    const int issuer = 32 * D0 + h * 128;  // lane 0 of the first drain warp of each half: bulk-store issue
     uint32_t c = 0;
     for (int u = ubase; u < nunits; u += ustep) {
       const Unit w = unit_of(u, ep, ntn, ntm, nkb_all, BN, BMU);
@@ -936,10 +970,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kc = 0; kc < w.nkb; kc += kChunkKB, ++c) {
         const int buf = c % C::kAccBufs;
         mbar_wait(afull0 + 8 * buf, (c / C::kAccBufs) & 1);
-        if (warp == 6 && lane == 0) TRACE(5, c);
+        if (warp == D0 && lane == 0) TRACE(5, c);
         tc_fence_after();
 #ifndef ESGD_X_NODRAIN
-        if (HB <= 64) {
+        if (HB <= 64 && NS == 4) {  // (the 8-split-warp CTA keeps 96 registers: 16-column loads)
 #pragma unroll
           for (int c0 = 0; c0 < HB; c0 += 32) {
             uint32_t v[32];
@@ -948,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) racc[c0 + j] = __fadd_rn(racc[c0 + j], __uint_as_float(v[j]));
           }
-        } else {  // BN = 192: 96 accumulators per thread leave room for 16-column loads only
+        } else {  // BN = 192 (96 accumulators per thread), or the 8-split-warp CTA at 96 registers: 16-column loads
 #pragma unroll
           for (int c0 = 0; c0 < HB; c0 += 16) {
             float v[16];
@@ -964,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (PAIR) mbar_arrive_leader(aempty0 + 8 * buf);
           else mbar_arrive(aempty0 + 8 * buf);
         }
-        if (warp == 6 && lane == 0) TRACE(6, c);
+        if (warp == D0 && lane == 0) TRACE(6, c);
       }
       const int m0 = w.m0 + arow;  // this CTA's rows of the unit
       const int row = m0 + q * 32 + lane;
@@ -1243,7 +1277,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(cta_threads(BN, SPLIT));
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -1257,7 +1291,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
     ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: cluster launch: %s", cudaGetErrorString(e));
   } else {
     const int grid = (int)std::min<int64_t>(units, kNumSMs);
-    k_tc_gemm<BN, SPLIT, AMN, BMN, false, GM><<<grid, kThreads, C::kSmemBytes, st>>>(ma, mb, mc, ep, ga);
+    k_tc_gemm<BN, SPLIT, AMN, BMN, false, GM><<<grid, cta_threads(BN, SPLIT), C::kSmemBytes, st>>>(ma, mb, mc, ep, ga);
   }
   if (splits > 1) {
     dim3 rg(stride_grid((int64_t)d->m * d->n, 256, 8), d->batch);
