@@ -372,16 +372,26 @@ def run_device(args):
         desc, fl, t, prec, tkey = dom
         tf32_peak = pk.get("bf16_tflops", 1590.0) / 2
         ach = prec * fl / t / 1e12
+        # achieved = ALGORITHMIC flops (2MNK, the fp32 product the GEMM delivers) per
+        # launch / launch time, against the tensor-core peak of the kind the kernel
+        # issues (tf32 = bf16 / 2). 3xTF32 issues 3 tf32 MMAs per product, so the
+        # algorithmic fraction is at most 1/3; the same launch is also given as a
+        # fraction of the 3xTF32 emulation peak (peak / 3) and of the kind::tf32
+        # issue-rate floor (tensor-pipe work = 3 x algorithmic)
+        alg = fl / t / 1e12
+        floor = 148 * 4096 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         roof = {"kernel": f"esgd_tc_gemm_f32 (k_tc_gemm, {desc})", "bound": "tensor",
-                "achieved": round(ach, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
-                "frac": round(ach / tf32_peak, 4), "traffic": traffic(tkey, args.model),
-                "fp32_equivalent_tflops": round(fl / t / 1e12, 1), "launch_s": t,
-                "algorithmic_flops_per_launch": fl,
+                "achieved": round(alg, 1), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                "frac": round(alg / tf32_peak, 4), "traffic": traffic(tkey, args.model),
+                "launch_s": t, "algorithmic_flops_per_launch": fl,
                 "peak_source": f"{src} bf16_tflops / 2 (tf32 = half the bf16 rate)",
+                "emulation_peak_tflops": round(tf32_peak / prec, 1),
+                "frac_of_emulation_peak": round(alg * prec / tf32_peak, 4),
+                "tf32_pipe_tflops": round(ach, 1),
                 # the issue-rate floor of kind::tf32 MMAs (4096 flop/cycle/SM, measured at the
                 # floor in isolation by tools/probe_mma_rate.cu) at the max SM clock
-                "tensor_floor_tflops": round(148 * 4096 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, 1),
-                "frac_of_floor": round(ach / (148 * 4096 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12), 4)}
+                "tensor_floor_tflops": round(floor, 1),
+                "frac_of_floor": round(ach / floor, 4)}
     else:  # no GEMM reaches the tensor-core threshold (LeNet): the round is launch/latency-bound
         roof = dict(roof_upd, note="no tcgen05 GEMM in this round (all GEMMs below the tensor-core "
                     "threshold run on the FFMA kernel); the round is launch/latency-bound "
