@@ -33,6 +33,13 @@ SHAPES = [
     ("x.fc6.wgradT", 4096, 9216, 128, 0, 1, 1),
     ("x.conv2.dgrad.kmajor", 93312, 1600, 192, 0, 0, 1),
     ("x.conv2.dgrad.rowmajorC", 93312, 1600, 192, 1, 0, 0),
+    # forward convolutions as C^T = W . colT (the weights as the K-major A operand)
+    ("conv4.fwd", 21632, 256, 3456, 1, 0, 1),
+    ("x.conv4.fwdT", 256, 21632, 3456, 0, 1, 0),
+    ("conv5.fwd", 21632, 256, 2304, 1, 0, 1),
+    ("x.conv5.fwdT", 256, 21632, 2304, 0, 1, 0),
+    ("x.conv3.fwdT", 384, 21632, 1728, 0, 1, 0),
+    ("x.conv2.fwdT", 192, 93312, 1600, 0, 1, 0),
 ]
 
 

@@ -22,6 +22,20 @@ from paper_1708_02983_b200.device import stream_ptr  # noqa: E402
 from paper_1708_02983_b200.updates import sync_update_, sync_update_sum_  # noqa: E402
 
 
+def update_solo():
+    """the P = 1 round update (esgd_sync_update_solo_f32), 61.1M params"""
+    from paper_1708_02983_b200.updates import sync_update_solo_
+    n = 61_100_840
+    ld = (n + 63) // 64 * 64
+    W = torch.randn((1, ld), device="cuda")
+    G = torch.randn_like(W)
+    Cc = torch.randn(ld, device="cuda")
+    hy = HyperParams(eta=0.01, rho=0.1)
+    for _ in range(5):
+        sync_update_solo_(W, G, Cc, n, hy)
+    torch.cuda.synchronize()
+
+
 def update(fused=False):
     n = 61_100_840
     ld = (n + 63) // 64 * 64
@@ -94,6 +108,8 @@ if __name__ == "__main__":
     case = sys.argv[1]
     if case == "update":
         update()
+    elif case == "update_solo":
+        update_solo()
     elif case == "update_sum":
         update(fused=True)
     elif case == "dgrad":
