@@ -369,6 +369,16 @@ int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* 
                          const float* mask, int64_t mask_sb, int32_t k, int32_t stride,
                          int32_t pad, int32_t batch, esgd_stream_t stream);
 
+/* the same with the relu backward of the pool's input fused, gated by the
+ * pooled output y (stride y_sb between replicas) of a window that selected
+ * the pixel — that window's max is the pixel's own value, so the result is
+ * bitwise the mask=input form while reading the pooled output instead of the
+ * input. Replaces network.py:197-199's act' for conv->relu->pool stacks.     */
+int esgd_maxpool_bwd_relu_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
+                              esgd_tensor4 yd, int64_t dy_sb, const int32_t* argmax, const float* y,
+                              int64_t y_sb, int32_t k, int32_t stride, int32_t pad, int32_t batch,
+                              esgd_stream_t stream);
+
 /* strided 4-D copy (layout change, e.g. NHWC -> NCHW flatten for the FC
  * head and back), optional relu mask on the source (src>0 of mask).         */
 int esgd_copy4_f32(float* dst, esgd_tensor4 dd, int64_t d_sb, const float* src, esgd_tensor4 sd,

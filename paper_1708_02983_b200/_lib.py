@@ -132,6 +132,7 @@ _SIGS = {
     "esgd_rowsum_f32": (C.c_int, [vp, i64, vp, i64, i64, i32, i64, i32, vp, vp]),
     "esgd_maxpool_fwd_f32": (C.c_int, [vp, Tensor4, i64, vp, vp, Tensor4, i64, i32, i32, i32, i32, vp]),
     "esgd_maxpool_bwd_f32": (C.c_int, [vp, Tensor4, i64, vp, Tensor4, i64, vp, vp, i64, i32, i32, i32, i32, vp]),
+    "esgd_maxpool_bwd_relu_f32": (C.c_int, [vp, Tensor4, i64, vp, Tensor4, i64, vp, vp, i64, i32, i32, i32, i32, vp]),
     "esgd_copy4_f32": (C.c_int, [vp, Tensor4, i64, vp, Tensor4, i64, i32, vp]),
 }
 

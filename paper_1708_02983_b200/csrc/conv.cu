@@ -374,17 +374,32 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_sq(float* __restrict__ y, e
 // thread loads 4 argmax + 4 dy values per channel for 4 outputs (the per-pixel
 // gather loads 8 per pixel). Each pixel still sums its windows in (oy, ox)
 // order, so results equal k_maxpool_bwd_t's.
-template <int K>
-__global__ void __launch_bounds__(256) k_maxpool_bwd_s2(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+// GATE fuses the relu backward of the pool's input: 1 = the input itself
+// (gsrc laid out as dx) > 0; 2 = the pooled output (laid out as dy) > 0 of a
+// window that selected the pixel — that window's max is the pixel's own
+// value, and a pixel gets a nonzero sum only through such a window, so 2
+// gives 1's bits while reading the 4x smaller output. Every load of a channel
+// is issued before any is used, two channels per iteration: the kernel is
+// load-latency bound otherwise (ncu: 17% of DRAM bandwidth with the gate
+// loads issued behind the argmax compares).
+#ifndef ESGD_POOL_MINB
+#define ESGD_POOL_MINB 4
+#endif
+#ifndef ESGD_POOL_UNROLL
+#define ESGD_POOL_UNROLL 2
+#endif
+constexpr int kPoolUnroll = ESGD_POOL_UNROLL;
+template <int K, int GATE>
+__global__ void __launch_bounds__(256, ESGD_POOL_MINB) k_maxpool_bwd_s2(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                         const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                         const int32_t* __restrict__ amax,
-                                                        const float* __restrict__ mask, int64_t mask_sb, int grp) {
+                                                        const float* __restrict__ gsrc, int64_t g_sb, int grp) {
   const int z = blockIdx.z;
   const int bh = (xd.h + 1) / 2, bw = (xd.w + 1) / 2, nb = bh * bw, ohw = yd.h * yd.w;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= xd.n * nb) return;
   const int img = q / nb, r = q - img * nb, a = r / bw, b = r - a * bw;
-  // window slots: 0 (a-1,b-1) 1 (a-1,b) 2 (a,b-1) 3 (a,b); K = 2 uses slot 3 only
+  // window slots t = (ti, tj): output (a - 1 + ti, b - 1 + tj); K = 2 uses slot 3 only
   bool wok[4];
   int wo[4], yo[4];
 #pragma unroll
@@ -394,61 +409,60 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_s2(float* __restrict__ dx, 
     wo[t] = oy * yd.w + ox;
     yo[t] = oy * yd.sh + ox * yd.sw;
   }
+  // block pixels i = (di, dj): input (2a + di, 2b + dj)
   const int iy0 = 2 * a, ix0 = 2 * b;
   const bool pok[4] = {true, ix0 + 1 < xd.w, iy0 + 1 < xd.h, iy0 + 1 < xd.h && ix0 + 1 < xd.w};
+  const int64_t xo[4] = {0, xd.sw, xd.sh, xd.sh + xd.sw};
+  const int p00 = iy0 * xd.w + ix0;
+  const int pidx[4] = {p00, p00 + 1, p00 + xd.w, p00 + xd.w + 1};
   const int c0 = blockIdx.y * grp, c1 = min(xd.c, c0 + grp);
   const int32_t* ap = amax + z * ((int64_t)yd.n * yd.c * ohw) + ((int64_t)img * yd.c + c0) * ohw;
-  const float* dyp = dy + z * y_sb + img * yd.sn + (int64_t)c0 * yd.sc;
+  const int64_t yoff = img * yd.sn + (int64_t)c0 * yd.sc;
+  const float* dyp = dy + z * y_sb + yoff;
   const int64_t o0 = img * xd.sn + (int64_t)c0 * xd.sc + iy0 * xd.sh + ix0 * xd.sw;
   float* dxp = dx + z * x_sb + o0;
-  const float* mp = mask ? mask + z * mask_sb + o0 : nullptr;
-  const int p00 = iy0 * xd.w + ix0;
+  const float* gp = GATE == 1 ? gsrc + z * g_sb + o0 : GATE == 2 ? gsrc + z * g_sb + yoff : nullptr;
+  const int64_t gstep = GATE == 1 ? xd.sc : yd.sc;
+#pragma unroll kPoolUnroll
   for (int c = c0; c < c1; ++c) {
     int am[4];
-    float d[4];
+    float d[4], gv[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       am[t] = wok[t] ? __ldg(ap + wo[t]) : -1;
       d[t] = wok[t] ? __ldg(dyp + yo[t]) : 0.f;
-    }
-    // pixel (dy, dx) of the block: covered by slots with (slot row >= dy... ):
-    // (0,0): 0,1,2,3  (0,1): 1,3  (1,0): 2,3  (1,1): 3   [K = 3]
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    if (K == 3) {
-      if (am[0] == p00) acc[0] += d[0];
-      if (am[1] == p00) acc[0] += d[1];
-      if (am[2] == p00) acc[0] += d[2];
-      if (am[3] == p00) acc[0] += d[3];
-      if (am[1] == p00 + 1) acc[1] += d[1];
-      if (am[3] == p00 + 1) acc[1] += d[3];
-      if (am[2] == p00 + xd.w) acc[2] += d[2];
-      if (am[3] == p00 + xd.w) acc[2] += d[3];
-      if (am[3] == p00 + xd.w + 1) acc[3] += d[3];
-    } else {
-      if (am[3] == p00) acc[0] += d[3];
-      if (am[3] == p00 + 1) acc[1] += d[3];
-      if (am[3] == p00 + xd.w) acc[2] += d[3];
-      if (am[3] == p00 + xd.w + 1) acc[3] += d[3];
+      if (GATE == 2) gv[t] = wok[t] ? __ldg(gp + yo[t]) : 0.f;
+      if (GATE == 1) gv[t] = pok[t] ? __ldg(gp + xo[t]) : 0.f;
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (!pok[t]) continue;
-      const int64_t off = (t >> 1) * xd.sh + (t & 1) * xd.sw;
-      float v = acc[t];
-      if (mp) v = __fmul_rn(v, mp[off] > 0.f ? 1.f : 0.f);
-      dxp[off] = v;
+    for (int i = 0; i < 4; ++i) {
+      float acc = 0.f;
+      bool pos = false;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        // slot t's window covers pixel i iff di <= ti and dj <= tj (K = 3)
+        const bool cov = K == 3 ? ((i >> 1) <= (t >> 1) && (i & 1) <= (t & 1)) : t == 3;
+        if (cov && am[t] == pidx[i]) {
+          acc += d[t];
+          if (GATE == 2) pos = pos || gv[t] > 0.f;
+        }
+      }
+      if (GATE == 1) acc = __fmul_rn(acc, gv[i] > 0.f ? 1.f : 0.f);
+      if (GATE == 2) acc = __fmul_rn(acc, pos ? 1.f : 0.f);
+      if (pok[i]) dxp[xo[i]] = acc;
     }
     ap += ohw;
     dyp += yd.sc;
     dxp += xd.sc;
-    if (mp) mp += xd.sc;
+    if (GATE) gp += gstep;
   }
 }
 
 __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                        const float* __restrict__ dy, esgd_tensor4 yd, int64_t y_sb,
                                                        const int32_t* __restrict__ amax,
-                                                       const float* __restrict__ mask, int64_t mask_sb, int k,
+                                                       const float* __restrict__ mask, int64_t mask_sb,
+                                                       const float* __restrict__ ymask, int64_t ym_sb, int k,
                                                        int stride, int pad, int grp) {
   const int z = blockIdx.z;
   const int hw = xd.h * xd.w, npin = xd.n * hw, ohw = yd.h * yd.w;
@@ -479,6 +493,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
     const int64_t o0 = z * x_sb + img * xd.sn + (int64_t)c0 * xd.sc + iy * xd.sh + ix * xd.sw;
     float* dxp = dx + o0;
     const float* mp = mask ? mask + z * mask_sb + (o0 - z * x_sb) : nullptr;
+    const float* ymp = ymask ? ymask + z * ym_sb + img * yd.sn + (int64_t)c0 * yd.sc : nullptr;
 #pragma unroll 2
     for (int c = c0; c < c1; ++c) {
       int a[4];
@@ -488,13 +503,20 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
         a[t] = ok[t] ? __ldg(ap + wo[t]) : -1;
         d[t] = ok[t] ? __ldg(dyp + yo[t]) : 0.f;
       }
-      float acc = 0.f;
+      float acc = 0.f, g = 0.f;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (a[t] == p) acc += d[t];
+        if (a[t] == p) {
+          acc += d[t];
+          if (ymp && __ldg(ymp + yo[t]) > 0.f) g = 1.f;
+        }
       if (mp) {
         acc = __fmul_rn(acc, *mp > 0.f ? 1.f : 0.f);
         mp += xd.sc;
+      }
+      if (ymp) {
+        acc = __fmul_rn(acc, g);
+        ymp += yd.sc;
       }
       *dxp = acc;
       ap += ohw;
@@ -506,78 +528,16 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd_t(float* __restrict__ dx, e
   for (int c = c0; c < c1; ++c) {
     const int32_t* ap = amax + z * ytotal + ((int64_t)img * yd.c + c) * ohw;
     const float* dyp = dy + z * y_sb + img * yd.sn + c * yd.sc;
-    float acc = 0.f;
+    float acc = 0.f, g = 0.f;
     for (int oy = oy_lo; oy <= oy_hi; ++oy)
       for (int ox = ox_lo; ox <= ox_hi; ++ox)
-        if (ap[oy * yd.w + ox] == p) acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
+        if (ap[oy * yd.w + ox] == p) {
+          acc += __ldg(dyp + oy * yd.sh + ox * yd.sw);
+          if (ymask && __ldg(ymask + z * ym_sb + img * yd.sn + c * yd.sc + oy * yd.sh + ox * yd.sw) > 0.f) g = 1.f;
+        }
     const int64_t o = img * xd.sn + c * xd.sc + iy * xd.sh + ix * xd.sw;
     if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
-    dx[z * x_sb + o] = acc;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_maxpool_fwd(float* __restrict__ y, esgd_tensor4 yd,
-                                                     int64_t y_sb, int32_t* __restrict__ amax,
-                                                     const float* __restrict__ x, esgd_tensor4 xd,
-                                                     int64_t x_sb, int k, int stride, int pad) {
-  const int z = blockIdx.y;
-  const unsigned total = (unsigned)yd.n * yd.c * yd.h * yd.w;
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    unsigned t = e;
-    const int ox = (int)(t % (unsigned)yd.w); t /= (unsigned)yd.w;
-    const int oy = (int)(t % (unsigned)yd.h); t /= (unsigned)yd.h;
-    const int c = (int)(t % (unsigned)yd.c);
-    const int img = (int)(t / (unsigned)yd.c);
-    float best = -INFINITY;
-    int bi = -1;
-    for (int ky = 0; ky < k; ++ky) {
-      const int iy = oy * stride - pad + ky;
-      if (iy < 0 || iy >= xd.h) continue;
-      for (int kx = 0; kx < k; ++kx) {
-        const int ix = ox * stride - pad + kx;
-        if (ix < 0 || ix >= xd.w) continue;
-        const float v = __ldg(x + z * x_sb + off4(xd, img, c, iy, ix));
-        if (bi < 0 || v > best) { best = v; bi = iy * xd.w + ix; }
-      }
-    }
-    y[z * y_sb + off4(yd, img, c, oy, ox)] = best;
-    amax[(int64_t)z * total + e] = bi;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_maxpool_bwd(float* __restrict__ dx, esgd_tensor4 xd,
-                                                     int64_t x_sb, const float* __restrict__ dy,
-                                                     esgd_tensor4 yd, int64_t y_sb,
-                                                     const int32_t* __restrict__ amax,
-                                                     const float* __restrict__ mask, int64_t mask_sb, int k,
-                                                     int stride, int pad) {
-  const int z = blockIdx.y;
-  const unsigned total = (unsigned)xd.n * xd.c * xd.h * xd.w;
-  const int64_t ytotal = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    unsigned t = e;
-    const int ix = (int)(t % (unsigned)xd.w); t /= (unsigned)xd.w;
-    const int iy = (int)(t % (unsigned)xd.h); t /= (unsigned)xd.h;
-    const int c = (int)(t % (unsigned)xd.c);
-    const int img = (int)(t / (unsigned)xd.c);
-    const int me = iy * xd.w + ix;
-    // windows covering iy: oy*stride - pad <= iy <= oy*stride - pad + k - 1
-    int oy_lo = iy + pad - k + 1;
-    oy_lo = oy_lo <= 0 ? 0 : (oy_lo + stride - 1) / stride;
-    int oy_hi = (iy + pad) / stride;
-    if (oy_hi > yd.h - 1) oy_hi = yd.h - 1;
-    int ox_lo = ix + pad - k + 1;
-    ox_lo = ox_lo <= 0 ? 0 : (ox_lo + stride - 1) / stride;
-    int ox_hi = (ix + pad) / stride;
-    if (ox_hi > yd.w - 1) ox_hi = yd.w - 1;
-    float acc = 0.f;
-    for (int oy = oy_lo; oy <= oy_hi; ++oy)
-      for (int ox = ox_lo; ox <= ox_hi; ++ox) {
-        const unsigned ye = (((unsigned)img * yd.c + c) * yd.h + oy) * yd.w + ox;
-        if (amax[z * ytotal + ye] == me) acc += __ldg(dy + z * y_sb + off4(yd, img, c, oy, ox));
-      }
-    const int64_t o = off4(xd, img, c, iy, ix);
-    if (mask) acc = __fmul_rn(acc, mask[z * mask_sb + o] > 0.f ? 1.f : 0.f);
+    if (ymask) acc = __fmul_rn(acc, g);
     dx[z * x_sb + o] = acc;
   }
 }
@@ -767,16 +727,12 @@ extern "C" int esgd_maxpool_fwd_f32(float* y, esgd_tensor4 yd, int64_t y_sb, int
       k_maxpool_fwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad, gp);
     return check_launch("esgd_maxpool_fwd_f32");
   }
-  int64_t total = (int64_t)yd.n * yd.c * yd.h * yd.w;
-  dim3 grid(stride_grid(total, 256, 16), batch);
-  k_maxpool_fwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(y, yd, y_sb, argmax, x, xd, x_sb, k, stride, pad);
-  return check_launch("esgd_maxpool_fwd_f32");
 }
 
-extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
-                                    esgd_tensor4 yd, int64_t y_sb, const int32_t* argmax,
-                                    const float* mask, int64_t mask_sb, int32_t k, int32_t stride,
-                                    int32_t pad, int32_t batch, esgd_stream_t stream) {
+static int maxpool_bwd(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy, esgd_tensor4 yd, int64_t y_sb,
+                       const int32_t* argmax, const float* mask, int64_t mask_sb, const float* ymask,
+                       int64_t ym_sb, int32_t k, int32_t stride, int32_t pad, int32_t batch,
+                       esgd_stream_t stream) {
   ESGD_REQUIRE(valid4(xd) && valid4(yd) && k >= 1 && stride >= 1 && pad >= 0 && batch >= 1 &&
                    yd.n == xd.n && yd.c == xd.c,
                ESGD_ERR_SHAPE, "maxpool_bwd: bad geometry");
@@ -787,23 +743,44 @@ extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, co
     const int64_t nblk = (int64_t)xd.n * ((xd.h + 1) / 2) * ((xd.w + 1) / 2);
     const int gp = pick_group(nblk * batch, xd.c);
     dim3 g2((unsigned)((nblk + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);
-    if (k == 3)
-      k_maxpool_bwd_s2<3><<<g2, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, gp);
-    else
-      k_maxpool_bwd_s2<2><<<g2, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, gp);
+    const float* gs = ymask ? ymask : mask;
+    const int64_t gsb = ymask ? ym_sb : mask_sb;
+    const int gate = ymask ? 2 : mask ? 1 : 0;
+    cudaStream_t st = ESGD_STREAM(stream);
+#define ESGD_POOL_S2(KK, GG) \
+  k_maxpool_bwd_s2<KK, GG><<<g2, 256, 0, st>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, gs, gsb, gp)
+    if (k == 3) {
+      if (gate == 2) ESGD_POOL_S2(3, 2);
+      else if (gate == 1) ESGD_POOL_S2(3, 1);
+      else ESGD_POOL_S2(3, 0);
+    } else {
+      if (gate == 2) ESGD_POOL_S2(2, 2);
+      else if (gate == 1) ESGD_POOL_S2(2, 1);
+      else ESGD_POOL_S2(2, 0);
+    }
+#undef ESGD_POOL_S2
     return check_launch("esgd_maxpool_bwd_f32");
   }
-  {
-    const int gp = pick_group((int64_t)xd.n * xd.h * xd.w * batch, xd.c);
-    dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);
-    dim3 b2(256);
-    k_maxpool_bwd_t<<<g2, b2, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad, gp);
-    return check_launch("esgd_maxpool_bwd_f32");
-  }
-  int64_t total = (int64_t)xd.n * xd.c * xd.h * xd.w;
-  dim3 grid(stride_grid(total, 256, 16), batch);
-  k_maxpool_bwd<<<grid, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, k, stride, pad);
+  const int gp = pick_group((int64_t)xd.n * xd.h * xd.w * batch, xd.c);
+  dim3 g2((unsigned)(((int64_t)xd.n * xd.h * xd.w + 255) / 256), (unsigned)((xd.c + gp - 1) / gp), batch);
+  k_maxpool_bwd_t<<<g2, 256, 0, ESGD_STREAM(stream)>>>(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, ymask,
+                                                       ym_sb, k, stride, pad, gp);
   return check_launch("esgd_maxpool_bwd_f32");
+}
+
+extern "C" int esgd_maxpool_bwd_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
+                                    esgd_tensor4 yd, int64_t y_sb, const int32_t* argmax,
+                                    const float* mask, int64_t mask_sb, int32_t k, int32_t stride,
+                                    int32_t pad, int32_t batch, esgd_stream_t stream) {
+  return maxpool_bwd(dx, xd, x_sb, dy, yd, y_sb, argmax, mask, mask_sb, nullptr, 0, k, stride, pad, batch, stream);
+}
+
+extern "C" int esgd_maxpool_bwd_relu_f32(float* dx, esgd_tensor4 xd, int64_t x_sb, const float* dy,
+                                         esgd_tensor4 yd, int64_t dy_sb, const int32_t* argmax, const float* y,
+                                         int64_t y_sb, int32_t k, int32_t stride, int32_t pad, int32_t batch,
+                                         esgd_stream_t stream) {
+  ESGD_REQUIRE(y, ESGD_ERR_INPUT, "maxpool_bwd_relu: null pooled output");
+  return maxpool_bwd(dx, xd, x_sb, dy, yd, dy_sb, argmax, nullptr, 0, y, y_sb, k, stride, pad, batch, stream);
 }
 
 extern "C" int esgd_copy4_f32(float* dst, esgd_tensor4 dd, int64_t d_sb, const float* src,

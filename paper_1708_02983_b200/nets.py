@@ -461,10 +461,16 @@ class DeviceNet:
                 lay = L.lay
                 yd = self._out_desc(i)
                 dnext = self._other(dcur)
-                mask = xin if pact == 1 else None
-                _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd, d_sb,
-                                                    self.amax[i].data_ptr(), mask, x_sb, lay.k, lay.stride,
-                                                    lay.pad, nb, stream), "maxpool_bwd")
+                if pact == 1:  # relu' of the pool input, read off the (4x smaller) pooled output
+                    yo = self.outs[i]
+                    _lib.check(lib.esgd_maxpool_bwd_relu_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(),
+                                                             yd, d_sb, self.amax[i].data_ptr(), yo.data_ptr(),
+                                                             yo.stride(0), lay.k, lay.stride, lay.pad, nb, stream),
+                               "maxpool_bwd_relu")
+                else:
+                    _lib.check(lib.esgd_maxpool_bwd_f32(dnext.data_ptr(), xd, dnext.stride(0), dcur.data_ptr(), yd,
+                                                        d_sb, self.amax[i].data_ptr(), None, 0, lay.k, lay.stride,
+                                                        lay.pad, nb, stream), "maxpool_bwd")
                 dcur = dnext
             elif L.implicit:  # conv as implicit GEMMs; delta is CNHW [Cout][np4]
                 lay = L.lay

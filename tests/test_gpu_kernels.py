@@ -458,3 +458,102 @@ def test_tcgen05_gemm_wide_tiles_and_orientation(m, n, k, a_major, b_major, bias
     if bias:
         ref = np.maximum(ref + bvec.astype(np.float64), 0.0)
     assert rel_err(host(Cd), ref) < 3e-6, rel_err(host(Cd), ref)
+
+
+@pytest.mark.parametrize("k,s,p,h,w", [(3, 2, 0, 55, 55), (3, 2, 0, 14, 9), (2, 2, 0, 7, 8), (3, 2, 1, 16, 16),
+                                       (3, 2, 1, 15, 17), (3, 1, 1, 9, 10), (2, 1, 0, 6, 5), (4, 3, 1, 20, 19)])
+def test_maxpool_bwd_relu_equals_input_mask_bitwise(k, s, p, h, w):
+    """esgd_maxpool_bwd_relu_f32 (relu' gated by the pooled output) == the
+    input-mask form esgd_maxpool_bwd_f32(mask = x) bit for bit, both stride-2
+    and generic paths, two replicas, ties and ReLU zeros in the input"""
+    rng = np.random.default_rng(k * 10000 + s * 1000 + p * 100 + h + w)
+    n, c, reps = 2, 3, 2
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    plane, oplane = (n * h * w + 3) // 4 * 4, (n * oh * ow + 3) // 4 * 4
+    xs = [np.maximum(rng.standard_normal((n, c, h, w)), 0).astype(np.float32) for _ in range(reps)]
+    xs[0][0, 0, :5, :5] = 0.5
+    xs[1][1, 2] = 0.0  # an all-zero plane: every window's max is 0
+    xd = dev(np.stack([_cnhw(x, plane) for x in xs]))
+    y = torch.zeros((reps, c, oplane), device="cuda")
+    am = torch.zeros((reps, n, c, oh, ow), dtype=torch.int32, device="cuda")
+    yd4, xd4 = _lib.cnhw(n, c, oh, ow, oplane), _lib.cnhw(n, c, h, w, plane)
+    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), yd4, c * oplane, am.data_ptr(), xd.data_ptr(), xd4, c * plane,
+              k, s, p, reps, stream_ptr())
+    dyd = dev(np.stack([_cnhw(rng.standard_normal((n, c, oh, ow)).astype(np.float32), oplane) for _ in range(reps)]))
+    dx0 = torch.full((reps, c, plane), 7.0, device="cuda")
+    dx1 = torch.full((reps, c, plane), 7.0, device="cuda")
+    _lib.call("esgd_maxpool_bwd_f32", dx0.data_ptr(), xd4, c * plane, dyd.data_ptr(), yd4, c * oplane, am.data_ptr(),
+              xd.data_ptr(), c * plane, k, s, p, reps, stream_ptr())
+    _lib.call("esgd_maxpool_bwd_relu_f32", dx1.data_ptr(), xd4, c * plane, dyd.data_ptr(), yd4, c * oplane,
+              am.data_ptr(), y.data_ptr(), c * oplane, k, s, p, reps, stream_ptr())
+    npix = n * h * w
+    assert torch.equal(dx0[:, :, :npix].view(torch.int32), dx1[:, :, :npix].view(torch.int32))
+
+
+@pytest.mark.parametrize("k,s,p,h,w", [(3, 2, 0, 13, 13), (2, 2, 0, 8, 7), (3, 2, 1, 15, 17), (3, 1, 1, 9, 10)])
+@pytest.mark.parametrize("gate", ["none", "mask", "relu"])
+def test_maxpool_bwd_strided_layouts(k, s, p, h, w, gate):
+    """NHWC planes (not the dense rows the tile kernel stages) take the
+    register-gather kernels: bit-exact vs the oracle, each gating form"""
+    rng = np.random.default_rng(k * 100 + s * 10 + p + h * w)
+    n, c = 2, 3
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    x = np.maximum(rng.standard_normal((n, c, h, w)), -0.2).astype(np.float32)
+    xd4, yd4 = _lib.nhwc(n, c, h, w), _lib.nhwc(n, c, oh, ow)
+    xdev = dev(np.ascontiguousarray(x.transpose(0, 2, 3, 1)))
+    y = torch.zeros((n, oh, ow, c), device="cuda")
+    am = torch.zeros((n, c, oh, ow), dtype=torch.int32, device="cuda")
+    _lib.call("esgd_maxpool_fwd_f32", y.data_ptr(), yd4, 0, am.data_ptr(), xdev.data_ptr(), xd4, 0, k, s, p, 1,
+              stream_ptr())
+    ey, ea = O._maxpool(x, k, s, p)
+    assert np.array_equal(host(y).transpose(0, 3, 1, 2), ey) and np.array_equal(host(am), ea)
+    dy = rng.standard_normal((n, c, oh, ow)).astype(np.float32)
+    dyd = dev(np.ascontiguousarray(dy.transpose(0, 2, 3, 1)))
+    dx = torch.full((n, h, w, c), 7.0, device="cuda")
+    if gate == "relu":
+        _lib.call("esgd_maxpool_bwd_relu_f32", dx.data_ptr(), xd4, 0, dyd.data_ptr(), yd4, 0, am.data_ptr(),
+                  y.data_ptr(), 0, k, s, p, 1, stream_ptr())
+    else:
+        _lib.call("esgd_maxpool_bwd_f32", dx.data_ptr(), xd4, 0, dyd.data_ptr(), yd4, 0, am.data_ptr(),
+                  xdev.data_ptr() if gate == "mask" else None, 0, k, s, p, 1, stream_ptr())
+    exp = O._maxpool_bwd(dy, ea, (n, c, h, w))
+    if gate != "none":
+        exp = exp * (x > 0)
+    assert np.array_equal(host(dx).transpose(0, 3, 1, 2), exp)
+
+
+@pytest.mark.parametrize("m,n,k,batch,a_major,b_major", [
+    (1000, 1600, 192, 1, 1, 0),    # conv2 data-gradient class
+    (2048, 1024, 128, 1, 1, 0),    # FC weight-gradient class: K = batch
+    (300, 520, 160, 2, 0, 0),      # ragged M / N, two replicas
+    (129, 520, 40, 1, 0, 1),       # ragged K (two k-blocks, the second partial), N-major B
+    (197, 640, 96, 3, 1, 1),
+    (40000, 640, 192, 1, 1, 0),    # several waves of tiles
+])
+def test_tcgen05_gemm_short_k_many_n_tiles(m, n, k, batch, a_major, b_major):
+    """short-K GEMMs over many N tiles (conv2's data gradient and the FC
+    weight gradients are this class; ragged edges, replicas, every operand
+    major): within the 3xTF32 tolerance of fp64 and deterministic"""
+    rng = np.random.default_rng(m + 7 * n + 13 * k + batch)
+    A = rng.standard_normal((batch, m, k)).astype(np.float32)
+    B = rng.standard_normal((batch, n, k)).astype(np.float32)
+    As = np.ascontiguousarray(A.transpose(0, 2, 1)) if a_major else A
+    Bs = np.ascontiguousarray(B.transpose(0, 2, 1)) if b_major else B
+    lda = m if a_major else k
+    ldb = n if b_major else k
+    if lda % 4 or ldb % 4:
+        pytest.skip("TMA needs 16-B pitches")
+    Ad, Bd = dev(As), dev(Bs)
+    Cd = torch.full((batch, m, n), 5.0, device="cuda")
+    d = _lib.TcGemmDesc(m, n, k, batch, Ad.data_ptr(), lda, m * k, Bd.data_ptr(), ldb, n * k,
+                        Cd.data_ptr(), n, 1, m * n, None, 0, None, 0, 0, 0, 0, 0, 3,
+                        a_major, b_major, None, 0)
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    torch.cuda.synchronize()
+    for z in range(batch):
+        ref = _gemm_ref(A[z], B[z].T)
+        assert rel_err(host(Cd[z]), ref) < 3e-6, (z, rel_err(host(Cd[z]), ref))
+    C2 = torch.zeros_like(Cd)
+    d.c = C2.data_ptr()
+    _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
+    assert torch.equal(Cd, C2)

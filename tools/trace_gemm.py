@@ -30,7 +30,7 @@ def main():
         bench_conv_gemm.main()  # the last launch is traced
     else:
         shape = next(s for s in bench_gemm.SHAPES if s[0] == name)
-        bench_gemm.run(*shape, int(sys.argv[2]) if len(sys.argv) > 2 else 3, reps=1)
+        bench_gemm.run(*shape, int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 3, reps=1)
     lib = _lib.load()
     lib.esgd_trace_copy.restype = C.c_int
     buf = np.zeros((8, 4096), dtype=np.uint64)
@@ -52,6 +52,12 @@ def main():
     print(f"  chunk complete interval            {d(np.diff(cdone[c[0]:c[-1] + 1])):8.0f}")
     print(f"  drain time (complete -> drained)   {d(drained[c] - cdone[c]):8.0f}")
     print(f"  MMA acquires buffer after drained  {d(acq[c[2:]] - drained[c[2:] - 2]) if len(c) > 2 else float('nan'):8.0f}")
+    if "--raw" in sys.argv:  # per-K-block stamps (relative to the first TMA issue), first 64 K blocks
+        t0 = tma[0]
+        for i in range(min(64, G)):
+            print(f"    g={i:3d} tma {tma[i] - t0:8d} full {full[i] - t0:8d} split {split[i] - t0:8d} mma {mma[i] - t0:8d}")
+        for i in range(min(24, NC)):
+            print(f"    c={i:3d} acq {acq[i] - t0:8d} done {cdone[i] - t0:8d} drained {drained[i] - t0:8d}")
 
 
 if __name__ == "__main__":
