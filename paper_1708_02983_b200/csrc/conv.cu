@@ -140,8 +140,17 @@ __global__ void __launch_bounds__(256) k_im2col_t(float* __restrict__ col, int64
 // input/output pointers just advance, so an element costs one predicated load
 // and one coalesced store (the generic kernel spent ~60 instructions on
 // address math per element and was issue-bound at ~1.8 TB/s).
+#ifndef ESGD_IM2COL_MINB
+#define ESGD_IM2COL_MINB 6
+#endif
+#ifndef ESGD_COL2IM_MINB
+#define ESGD_COL2IM_MINB 4
+#endif
+#ifndef ESGD_POOLF_MINB
+#define ESGD_POOLF_MINB 8
+#endif
 template <int KS>
-__global__ void __launch_bounds__(256) k_im2col_sq(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
+__global__ void __launch_bounds__(256, ESGD_IM2COL_MINB) k_im2col_sq(float* __restrict__ col, int64_t col_sk, int64_t col_sb,
                                                    const float* __restrict__ x, esgd_tensor4 xd, int64_t x_sb,
                                                    int stride, int pad, int oh, int ow, int cgrp) {
   const int z = blockIdx.z;
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__(256) k_col2im_t(float* __restrict__ dx, esgd_t
 // 64 registers (4 CTAs/SM) for every KS: at 3x3 the uncapped 75 registers
 // allowed 3 (conv3-5 col2im 172 -> 156 us in total, tools/bench_conv.py).
 template <int KS>
-__global__ void __launch_bounds__(256, 4) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
+__global__ void __launch_bounds__(256, ESGD_COL2IM_MINB) k_col2im_sq(float* __restrict__ dx, esgd_tensor4 xd, int64_t x_sb,
                                                    const float* __restrict__ dcol, int64_t col_sk, int64_t col_sb,
                                                    int pad, int oh, int ow, const float* __restrict__ mask,
                                                    int64_t mask_sb, int grp) {
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd_t(float* __restrict__ y, es
 // thread, the channel loop only walks pointers; K*K independent loads per
 // channel, compared in (ky, kx) order with the generic kernel's tie rule
 template <int K>
-__global__ void __launch_bounds__(256) k_maxpool_fwd_sq(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
+__global__ void __launch_bounds__(256, ESGD_POOLF_MINB) k_maxpool_fwd_sq(float* __restrict__ y, esgd_tensor4 yd, int64_t y_sb,
                                                         int32_t* __restrict__ amax, const float* __restrict__ x,
                                                         esgd_tensor4 xd, int64_t x_sb, int stride, int pad, int grp) {
   const int z = blockIdx.z;
