@@ -41,11 +41,17 @@ from .network import Conv, ConvNetSpec, Dense, ModelSpec, Pool, view_table
 
 import os
 
-# a contraction goes to the tensor cores when M*N*K reaches this (below it
-# the fixed cost of a persistent tcgen05 launch exceeds the FFMA kernel's)
-# (measured on B200: LeNet's <=1e8-MAC GEMMs are faster on the split-K FFMA
-# kernel, every AlexNet contraction (>=5e8 MACs) on tcgen05)
-TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 28)))
+# a contraction goes to the tensor cores when M*N*K reaches this and its
+# operands suit TMA (a unit-stride dim, 16-B pitches); the rest take the
+# CUDA-core FFMA kernel. 2^27 MACs puts CIFAR-quick's convolutions (b = 64:
+# 1.6-4.2e8 MACs) and every AlexNet contraction on tcgen05 and keeps LeNet's
+# (<= 1.0e8) on FFMA. Measured (B200, bench.py, 1 worker, Sync round):
+# all-tcgen05 makes CIFAR-quick 0.409 -> 0.346 ms and LeNet 0.1886 -> 0.1823
+# ms, but LeNet's configs[0] trajectory is chaotic (ReLU / max-pool flips):
+# with 3xTF32's ~1e-6 GEMM error it leaves the fp32 envelope of the fp64 run
+# by round 20-50 (1.6e-5 vs the fp32 oracle's 9e-7, tests/test_gpu_parity.py),
+# so LeNet keeps the FFMA kernel's fp32-exact sums. ESGD_TC_MIN_MACS overrides.
+TC_MIN_FLOPS = int(os.environ.get("ESGD_TC_MIN_MACS", str(1 << 27)))
 # ESGD_IMPLICIT=1: tensor-core conv layers as implicit GEMMs (esgd_tc_conv_f32:
 # operands gathered from the activations, no im2col / col2im buffers). Off by
 # default: on AlexNet b=128 the gathered-operand GEMMs measured slower than

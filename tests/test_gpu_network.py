@@ -51,15 +51,18 @@ def _cnn_case(spec, layers, n, b, seed=0):
     return g_dev, g_ref
 
 
-@pytest.fixture(params=["tcgen05", "default", "implicit"])
+@pytest.fixture(params=["tcgen05", "default", "ffma", "implicit"])
 def gemm_routing(request, monkeypatch):
     """'tcgen05' sends every contraction above 4M MACs to the tensor-core
     kernel (so small test batches exercise it); 'default' is the engine's
-    production routing; 'implicit' additionally runs those conv layers as
-    implicit GEMMs (esgd_tc_conv_f32, no im2col / col2im)."""
+    production routing; 'ffma' forces the CUDA-core FFMA kernel; 'implicit'
+    additionally runs the tensor-core conv layers as implicit GEMMs
+    (esgd_tc_conv_f32, no im2col / col2im)."""
     from paper_1708_02983_b200 import nets
     if request.param in ("tcgen05", "implicit"):
         monkeypatch.setattr(nets, "TC_MIN_FLOPS", 1 << 22)
+    if request.param == "ffma":
+        monkeypatch.setattr(nets, "TC_MIN_FLOPS", 1 << 62)
     if request.param == "implicit":
         monkeypatch.setattr(nets, "IMPLICIT", True)
     return request.param

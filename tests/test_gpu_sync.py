@@ -97,8 +97,8 @@ def test_sync_cnn_multi_replica_vs_oracle(model, tc, monkeypatch):
     2e-8 / 3e-8 for LeNet / CIFAR-quick; the fp32 oracle is 4e-8 from fp64)."""
     from paper_1708_02983_b200 import network, nets
 
-    if tc:
-        monkeypatch.setattr(nets, "TC_MIN_FLOPS", 1 << 22)
+    # tc: contractions above 4M MACs on tcgen05; else all on the FFMA kernel
+    monkeypatch.setattr(nets, "TC_MIN_FLOPS", (1 << 22) if tc else (1 << 62))
     spec = network.MODELS[model](seed=1)
     layers = {"lenet": O.LENET, "cifar-quick": O.CIFAR_QUICK}[model]
     rng = np.random.default_rng(7)
