@@ -288,6 +288,19 @@ typedef struct {
 } esgd_conv_gather;
 int esgd_tc_conv_f32(const esgd_tc_gemm_desc* desc, const esgd_conv_gather* gather, int32_t side,
                      esgd_stream_t stream);
+/* The same implicit GEMM with the gathered operand loaded by TMA in im2col
+ * mode (cp.async.bulk.tensor...im2col) from an NHWC source: src is [n][y][x][c]
+ * (c innermost; replicas stacked along n: src_sb = images*src_h*src_w*c),
+ * `channels` a multiple of 32, K ordered (kh, kw, c) — one k-block is 32
+ * channels of one window tap, so the tile lands in the same 128-B-swizzled
+ * layout as a TMA-tiled operand. Forward window only: sgn = 1, yoff = xoff =
+ * -pad, grid = the window's output grid at `stride` (<= 8). side 1: A[m][k]
+ * (m = grid pixel; forward, or a stride-1 data gradient as the forward conv
+ * of the NHWC output gradient with pad' = k-1-pad and flipped weights);
+ * side 2: B[n][k] (n = (kh, kw, c), k = grid pixel; weight gradient).
+ * plane / img_stride are unused. Split-K workspace: esgd_tc_conv_ws_floats. */
+int esgd_tc_conv_tma_f32(const esgd_tc_gemm_desc* desc, const esgd_conv_gather* gather, int32_t side,
+                         esgd_stream_t stream);
 /* split-K workspace floats esgd_tc_conv_f32 needs for `desc` (0: no split). */
 int esgd_tc_conv_ws_floats(const esgd_tc_gemm_desc* desc, int64_t* floats);
 

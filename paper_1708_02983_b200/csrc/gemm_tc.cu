@@ -142,6 +142,18 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// TMA im2col load (4-D NHWC source, c innermost): `pixels` consecutive output
+// positions of the map's traversal starting at (w, h, n), channels c0.., each
+// read at that position + (off_w, off_h) — one k-block of an implicit GEMM
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int w,
+                                                int h, int n, int off_w, int off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(w), "r"(h), "r"(n),
+      "h"((unsigned short)off_w), "h"((unsigned short)off_h)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -355,6 +367,18 @@ struct Gather {
   int kdim;        // channels * KH * KW
   int hpitch;      // GM = 3: floats per channel of the smem halo
 };
+
+// GM = 4 / 5 (TMA im2col, NHWC source of SH x SW images, C = kdim / (KH*KW)
+// channels, K ordered (kh, kw, c)): the traversal position (w, h, n) of grid
+// pixel p (image n, row r, column c of the MH x MW grid) is
+// (c*stride + xoff, r*stride + yoff, n); yoff = xoff = -pad
+__device__ __forceinline__ void im2col_pos(const Gather& g, int p, int& w, int& h, int& n) {
+  const int hw = g.MH * g.MW;
+  n = p / hw;
+  const int r = p - n * hw, y = r / g.MW;
+  h = y * g.stride + g.yoff;
+  w = (r - y * g.MW) * g.stride + g.xoff;
+}
 
 // GM = 3 (halo): the source rows a unit's 128 pixels touch, as flattened
 // (image, y) rows of the channel planes, clamped to the planes
@@ -621,7 +645,8 @@ __global__ void __launch_bounds__(cta_threads(BN, SPLIT), 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               const __grid_constant__ CUtensorMap map_c, Epi ep, Gather ga) {
   using C = Cfg<BN, SPLIT, PAIR>;
-  static_assert(GM == 0 || (SPLIT && !AMN && !BMN), "gathered operands: 3xTF32, K-major partner");
+  static_assert(GM == 0 || (SPLIT && !AMN && (GM == 5 ? BMN : !BMN)),
+                "gathered operands: 3xTF32, K-major A; im2col B (GM = 5) is MN-major");
   constexpr int NS = split_warps(BN, SPLIT);   // split warps (warps 2 .. 1+NS)
   constexpr int KC = 32 / (NS / 4);            // K columns of an A row per split thread
   constexpr int D0 = 2 + NS;                   // first drain warp
@@ -706,9 +731,29 @@ __global__ void __launch_bounds__(cta_threads(BN, SPLIT), 1)
           } else {
             mbar_expect_tx(full0 + 8 * s, (GM == 1 ? 0 : kTileBytesA) + (GM == 2 ? 0 : C::kTileBytesB));
           }
-          if (GM == 0 || GM == 2)
+          if (GM == 0 || GM == 2 || GM == 5)
             load_operand<AMN, BM>(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, w.kb0 + kb, w.m0 + arow, w.z);
-          if (GM != 2)
+          if (GM == 4) {  // A = 128 grid pixels x 32 channels of one window tap
+            const int k0 = (w.kb0 + kb) * BK, cin = ga.kdim / (ga.KH * ga.KW);
+            const int tap = k0 / cin, c0 = k0 - tap * cin;
+            int iw, ih, in;
+            im2col_pos(ga, w.m0 + arow, iw, ih, in);
+            tma_load_im2col(smem_u32(st + C::kOffA), &map_a, full0 + 8 * s, c0, iw, ih,
+                            in + w.z * (ga.npix / (ga.MH * ga.MW)), tap % ga.KW, tap / ga.KW);
+          }
+          if (GM == 5) {  // B = 32 grid pixels (K) x 32 channels (N) boxes, one tap each, MN-major
+            const int cin = ga.kdim / (ga.KH * ga.KW);
+            int iw, ih, in;
+            im2col_pos(ga, (w.kb0 + kb) * BK, iw, ih, in);
+            in += w.z * (ga.npix / (ga.MH * ga.MW));
+#pragma unroll
+            for (int j = 0; j < C::kRowsB / 32; ++j) {
+              const int n = min(w.n0 + brow + 32 * j, ga.kdim - 32), tap = n / cin;
+              tma_load_im2col(smem_u32(st + C::kOffB) + j * 4096, &map_b, full0 + 8 * s, n - tap * cin, iw, ih, in,
+                              tap % ga.KW, tap / ga.KW);
+            }
+          }
+          if (GM != 2 && GM != 5)
             load_operand<BMN, C::kRowsB>(smem_u32(st + C::kOffB), &map_b, full0 + 8 * s, w.kb0 + kb,
                                          w.n0 + brow, w.z);
         }
@@ -1110,6 +1155,49 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+typedef CUresult (*PFN_encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeIm2col get_encode_im2col() {
+  static PFN_encodeIm2col fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeIm2col>(p);
+  }
+  return fn;
+}
+
+// im2col map over an NHWC source (c innermost) of nimg images, for GM = 4 /
+// 5: boxes of `pixels` traversal positions x 32 channels. The traversal box
+// per image runs from lower = (xoff, yoff) = -pad to (SW - 1, SH - 1) + upper,
+// upper = pad - (K - 1), in steps of the conv stride — the output grid
+// (CUTLASS make_im2col_tma_copy_desc uses the same corners).
+int make_im2col_map(CUtensorMap* map, const Gather& g, int64_t nimg, int pixels, bool atom32) {
+  auto enc = get_encode_im2col();
+  ESGD_REQUIRE(enc, ESGD_ERR_CUDA, "tc_conv_tma: cuTensorMapEncodeIm2col unavailable");
+  const int cin = g.kdim / (g.KH * g.KW);
+  cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)g.SW, (cuuint64_t)g.SH, (cuuint64_t)nimg};
+  cuuint64_t strides[3] = {(cuuint64_t)cin * 4, (cuuint64_t)g.SW * cin * 4, (cuuint64_t)g.SH * g.SW * cin * 4};
+  int lower[2] = {g.xoff, g.yoff};
+  int upper[2] = {-g.xoff - (g.KW - 1), -g.yoff - (g.KH - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.src), dims, strides, lower, upper,
+                   32, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ESGD_REQUIRE(r == CUDA_SUCCESS, ESGD_ERR_CUDA, "tc_conv_tma: cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  // drivers <= 13.1 encode a bit that breaks im2col loads from tensors under
+  // 128 KB (CUTLASS clears it the same way)
+  int drv = 0;
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 && (int64_t)nimg * strides[2] < 131072)
+    reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return ESGD_OK;
+}
+
 // 3-D map over an operand. K-major: dims (k, rows, batch), box (32, box_rows, 1).
 // MN-major: dims (rows, k, batch) with rows contiguous, box (32, 32, 1).
 int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64_t ld,
@@ -1231,11 +1319,20 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
   int rc = ESGD_OK;
-  if (GM == 0 || GM == 2) {  // (a gathered operand has no tensor map)
+  const int64_t nimg_all = (int64_t)(ga.npix / std::max(1, ga.MH * ga.MW)) * d->batch;
+  if (GM == 0 || GM == 2 || GM == 5) {  // (a gathered operand has no tensor map)
     rc = make_map(&ma, d->a, d->k, d->m, d->lda, d->batch, d->a_sb, BM, AMN, /*atom32=*/!SPLIT);
     if (rc) return rc;
   }
-  if (GM != 2) {
+  if (GM == 4) {
+    rc = make_im2col_map(&ma, ga, nimg_all, BM, /*atom32=*/false);
+    if (rc) return rc;
+  }
+  if (GM == 5) {
+    rc = make_im2col_map(&mb, ga, nimg_all, 32, /*atom32=*/true);
+    if (rc) return rc;
+  }
+  if (GM != 2 && GM != 5) {
     rc = make_map(&mb, d->b, d->k, d->n, d->ldb, d->batch, d->b_sb, C::kRowsB, BMN);
     if (rc) return rc;
   }
@@ -1316,6 +1413,14 @@ int launch_split(const Plan& p, cudaStream_t st) {
 template <int BN, int GM>
 int launch_gather(const Plan& p, cudaStream_t st, const Gather& ga) {
   return p.pair ? launch<BN, true, false, false, true, GM>(p, st, ga) : launch<BN, true, false, false, false, GM>(p, st, ga);
+}
+
+// TMA-im2col convolutions: GM = 4 loads A (K-major B), GM = 5 loads B (MN-major; K-major A)
+template <int BN, int GM>
+int launch_im2col(const Plan& p, cudaStream_t st, const Gather& ga) {
+  if (GM == 5)
+    return p.pair ? launch<BN, true, false, true, true, 5>(p, st, ga) : launch<BN, true, false, true, false, 5>(p, st, ga);
+  return p.pair ? launch<BN, true, false, false, true, 4>(p, st, ga) : launch<BN, true, false, false, false, 4>(p, st, ga);
 }
 
 int validate(const esgd_tc_gemm_desc* d) {
@@ -1452,6 +1557,63 @@ extern "C" int esgd_tc_conv_f32(const esgd_tc_gemm_desc* d, const esgd_conv_gath
   if (p.bn == 64) return tc::launch_gather<64, 2>(p, st, ga);
   if (p.bn == 192) return tc::launch_gather<192, 2>(p, st, ga);
   return tc::launch_gather<128, 2>(p, st, ga);
+}
+
+extern "C" int esgd_tc_conv_tma_f32(const esgd_tc_gemm_desc* d, const esgd_conv_gather* cg, int32_t side,
+                                    esgd_stream_t stream) {
+  using namespace esgd;
+  if (int rc = tc::validate(d)) return rc;
+  ESGD_REQUIRE(cg && (side == 1 || side == 2), ESGD_ERR_INPUT, "tc_conv_tma: gather descriptor and side 1|2 required");
+  ESGD_REQUIRE(d->precision == 3, ESGD_ERR_UNSUPPORTED, "tc_conv_tma: 3xTF32 only");
+  if (d->m == 0 || d->n == 0 || d->batch == 0) return ESGD_OK;
+  const int64_t kdim = (int64_t)cg->channels * cg->kh * cg->kw;
+  const int hw = cg->grid_h * cg->grid_w;
+  ESGD_REQUIRE(cg->src && cg->kh >= 1 && cg->kw >= 1 && cg->stride >= 1 && cg->stride <= 8 && cg->sgn == 1 &&
+                   cg->src_h >= 1 && cg->src_w >= 1 && hw >= 1 && cg->npix >= 1 && cg->npix % hw == 0 &&
+                   aligned16(cg->src),
+               ESGD_ERR_INPUT, "tc_conv_tma: bad gather geometry");
+  ESGD_REQUIRE(cg->channels % 32 == 0, ESGD_ERR_UNSUPPORTED,
+               "tc_conv_tma: channels must be a multiple of 32 (one k-block = 32 channels of one tap)");
+  // the traversal grid the map's corners define must be the conv's output grid
+  const int gw = (cg->src_w - 2 * cg->xoff - cg->kw) / cg->stride + 1;
+  const int gh = (cg->src_h - 2 * cg->yoff - cg->kh) / cg->stride + 1;
+  ESGD_REQUIRE(cg->xoff <= 0 && cg->yoff <= 0 && -cg->xoff < cg->kw && -cg->yoff < cg->kh && gw == cg->grid_w &&
+                   gh == cg->grid_h && cg->kw <= 128 && cg->kh <= 128,
+               ESGD_ERR_SHAPE, "tc_conv_tma: grid %dx%d is not the window's output grid %dx%d", cg->grid_h,
+               cg->grid_w, gh, gw);
+  const int64_t nimg = cg->npix / hw;
+  ESGD_REQUIRE(d->batch == 1 || cg->src_sb == nimg * cg->src_h * cg->src_w * cg->channels, ESGD_ERR_SHAPE,
+               "tc_conv_tma: replica NHWC sources must be contiguous (src_sb = images*H*W*C)");
+  if (side == 1) {
+    ESGD_REQUIRE(d->m == cg->npix && d->k == kdim, ESGD_ERR_SHAPE,
+                 "tc_conv_tma: im2col A is npix x kh*kw*channels (m=%d k=%d)", d->m, d->k);
+    ESGD_REQUIRE(d->b && d->b_major == 0 && (d->ldb & 3) == 0 && d->ldb >= d->k && aligned16(d->b),
+                 ESGD_ERR_SHAPE, "tc_conv_tma: B must be K-major with a 16-B aligned pitch");
+  } else {
+    ESGD_REQUIRE(d->n == kdim && d->k == cg->npix, ESGD_ERR_SHAPE,
+                 "tc_conv_tma: im2col B is kh*kw*channels x npix (n=%d k=%d)", d->n, d->k);
+    ESGD_REQUIRE(d->a && d->a_major == 0 && (d->lda & 3) == 0 && d->lda >= d->k && aligned16(d->a),
+                 ESGD_ERR_SHAPE, "tc_conv_tma: A must be K-major with a 16-B aligned pitch");
+  }
+  ESGD_REQUIRE(d->c, ESGD_ERR_INPUT, "tc_conv_tma: null output");
+  ESGD_REQUIRE(d->batch == 1 || ((d->a_sb & 3) == 0 && (d->b_sb & 3) == 0), ESGD_ERR_SHAPE,
+               "tc_conv_tma: batch strides must be multiples of 4");
+  tc::Gather ga{cg->src, cg->src_sb, 0, cg->src_h * cg->src_w * cg->channels, cg->src_h, cg->src_w, cg->grid_h,
+                cg->grid_w, cg->stride, cg->yoff, cg->xoff, 1, cg->kh, cg->kw, cg->npix, (int)kdim, 0};
+  const tc::Plan p = tc::make_plan(d, /*allow_swap=*/false);
+  const int64_t need = tc::ws_need(p);
+  ESGD_REQUIRE(need <= d->ws_floats, ESGD_ERR_UNSUPPORTED,
+               "tc_conv_tma: split-K workspace too small (need %lld floats, have %lld; size it with "
+               "esgd_tc_conv_ws_floats)", (long long)need, (long long)d->ws_floats);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (side == 1) {
+    if (p.bn == 64) return tc::launch_im2col<64, 4>(p, st, ga);
+    if (p.bn == 192) return tc::launch_im2col<192, 4>(p, st, ga);
+    return tc::launch_im2col<128, 4>(p, st, ga);
+  }
+  if (p.bn == 64) return tc::launch_im2col<64, 5>(p, st, ga);
+  if (p.bn == 192) return tc::launch_im2col<192, 5>(p, st, ga);
+  return tc::launch_im2col<128, 5>(p, st, ga);
 }
 
 extern "C" int esgd_tc_conv_ws_floats(const esgd_tc_gemm_desc* d, int64_t* floats) {

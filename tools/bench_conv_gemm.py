@@ -1,8 +1,10 @@
 """Implicit-GEMM convolutions (esgd_tc_conv_f32) on AlexNet b=128 layer
 shapes: forward, weight gradient, data gradient (CUDA events, warm).
 
-    python tools/bench_conv_gemm.py [--b 128] [--only conv2]
-Reports ms and fp32-equivalent TFLOP/s (2*M*N*K / t)."""
+    python tools/bench_conv_gemm.py [--b 128] [--only conv2] [--tma]
+Reports ms and fp32-equivalent TFLOP/s (2*M*N*K / t). --tma: the TMA
+im2col-mode variant (esgd_tc_conv_tma_f32, NHWC sources, K = (kh, kw, c)),
+plus the CNHW -> NHWC transposes it needs (esgd_transpose_f32)."""
 
 import argparse
 import ctypes as C
@@ -23,21 +25,29 @@ def r4(x):
     return (x + 3) // 4 * 4
 
 
+TMA = False
+
+
+def timed_fn(fn, reps=10):
+    for _ in range(3):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps / 1e3
+
+
 def timed(d, g, side, reps=10):
     lib = _lib.load()
     need = C.c_int64(0)
     _lib.check(lib.esgd_tc_conv_ws_floats(C.byref(d), C.byref(need)))
     ws = torch.zeros(max(4, need.value), device="cuda")
     d.ws, d.ws_floats = ws.data_ptr(), ws.numel()
-    for _ in range(3):
-        _lib.check(lib.esgd_tc_conv_f32(C.byref(d), C.byref(g), side, stream_ptr()))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        _lib.check(lib.esgd_tc_conv_f32(C.byref(d), C.byref(g), side, stream_ptr()))
-    e1.record()
-    e1.synchronize()
-    return e0.elapsed_time(e1) / reps / 1e3
+    fn = lib.esgd_tc_conv_tma_f32 if TMA else lib.esgd_tc_conv_f32
+    return timed_fn(lambda: _lib.check(fn(C.byref(d), C.byref(g), side, stream_ptr())), reps)
 
 
 def main():
@@ -45,7 +55,10 @@ def main():
     ap.add_argument("--b", type=int, default=128)
     ap.add_argument("--only", default="")
     ap.add_argument("--pass", dest="which", default="", help="fwd | wgrad | dgrad (default all)")
+    ap.add_argument("--tma", action="store_true")
     a = ap.parse_args()
+    global TMA
+    TMA = a.tma
     n = a.b
     tot = 0.0
     for name, cin, h, cout, k, s, p in LAYERS:
@@ -63,7 +76,21 @@ def main():
         dx = torch.empty(cin * xplane, device="cuda")
         bias = torch.randn(cout, device="cuda")
         npo, npi = n * oh * oh, n * h * h
-        gx = _lib.ConvGather(X.data_ptr(), 0, xplane, 0, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
+        if TMA and cin % 32:
+            continue
+        if TMA:  # NHWC copies of the input and of the output gradient
+            Xn = torch.empty(npi * cin, device="cuda")
+            Dn = torch.empty(npo * cout, device="cuda")
+            lib = _lib.load()
+            tx = timed_fn(lambda: _lib.check(lib.esgd_transpose_f32(Xn.data_ptr(), cin, 0, X.data_ptr(), xplane, 0,
+                                                                    cin, npi, 1, stream_ptr())))
+            td = timed_fn(lambda: _lib.check(lib.esgd_transpose_f32(Dn.data_ptr(), cout, 0, D.data_ptr(), oplane, 0,
+                                                                    cout, npo, 1, stream_ptr())))
+            print(f"{name}.nhwc  x {tx * 1e3:8.3f} ms  delta {td * 1e3:8.3f} ms", flush=True)
+            tot += tx + td
+            gx = _lib.ConvGather(Xn.data_ptr(), 0, 0, 0, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
+        else:
+            gx = _lib.ConvGather(X.data_ptr(), 0, xplane, 0, h, h, oh, oh, s, -p, -p, 1, k, k, npo, cin)
         d = _lib.TcGemmDesc(npo, cout, K, 1, None, 0, 0, W.data_ptr(), r4(K), 0, out.data_ptr(), 1, oplane, 0,
                             bias.data_ptr(), 0, None, 0, 0, 0, 1, 0, 3, 0, 0, None, 0)
         want = lambda kind: not a.which or a.which == kind
@@ -74,7 +101,11 @@ def main():
             rows.append(("wgrad", timed(d, gx, 2), 2.0 * npo * cout * K))
         if s == 1 and name != "conv1" and want("dgrad"):
             kd = cout * k * k
-            gd = _lib.ConvGather(D.data_ptr(), 0, oplane, 0, oh, oh, h, h, 1, p, p, -1, k, k, npi, cout)
+            if TMA:
+                q = k - 1 - p
+                gd = _lib.ConvGather(Dn.data_ptr(), 0, 0, 0, oh, oh, h, h, 1, -q, -q, 1, k, k, npi, cout)
+            else:
+                gd = _lib.ConvGather(D.data_ptr(), 0, oplane, 0, oh, oh, h, h, 1, p, p, -1, k, k, npi, cout)
             d = _lib.TcGemmDesc(npi, cin, kd, 1, None, 0, 0, Wp.data_ptr(), r4(kd), 0, dx.data_ptr(), 1, xplane, 0,
                                 None, 0, X.data_ptr(), 1, xplane, 0, 0, 0, 3, 0, 0, None, 0)
             rows.append(("dgrad", timed(d, gd, 1), 2.0 * npi * cin * kd))
