@@ -42,6 +42,12 @@ typedef void* esgd_comm_t; /* an NCCL communicator (ncclComm_t) */
 /* ---- library ----------------------------------------------------------- */
 const char* esgd_last_error(void);
 int esgd_abi_version(void);
+
+/* SMs the persistent tcgen05 GEMM / conv kernels leave free (grid = 148 -
+ * sms, rounded down to even) for a collective that runs beside them on
+ * dedicated SMs (esgd_center_step_nvls_f32 with ctas < 0). Process-wide,
+ * default 0; the tile plan and split-K counts (so the results) do not change. */
+int esgd_set_sm_reserve(int32_t sms);
 /* 1 if the library was built for sm_100a and a device of that class is present */
 int esgd_device_ok(int device);
 
@@ -103,8 +109,10 @@ int esgd_sync_update_nvls_f32(float* W, int64_t ldw, const float* G, int64_t ldg
 
 /* The same round split for overlap (what the engine runs): the center
  * slice (NVLS ld_reduce -> center step -> multicast broadcast) on a side
- * stream concurrently with the forward/backward (ctas = grid size, 0 = one
- * per SM), and the local worker step + next replica sum after it.          */
+ * stream concurrently with the forward/backward (ctas = grid size of small
+ * CTAs that sit next to the GEMM's, 0 = one per SM; ctas < 0: -ctas wide
+ * CTAs that take whole SMs, for use with esgd_set_sm_reserve), and the local
+ * worker step + next replica sum after it.                                  */
 int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, float* C_new_mc, int64_t n4,
                               int32_t world, int32_t rank, float etarho, int32_t num_workers, int32_t ctas,
                               esgd_stream_t stream);

@@ -120,6 +120,7 @@ _SIGS = {
     "esgd_async_wait": (C.c_int, [vp, i32, i32, vp, vp]),
     "esgd_tc_conv_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
     "esgd_tc_conv_tma_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
+    "esgd_set_sm_reserve": (C.c_int, [i32]),
     "esgd_tc_conv_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_tc_gemm_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_act_fwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),

@@ -3,7 +3,12 @@
 
 #include <string.h>
 
+#include <atomic>
+
 namespace esgd {
+
+static std::atomic<int> g_sm_reserve{0};
+int sm_reserve() { return g_sm_reserve.load(std::memory_order_relaxed); }
 
 static thread_local char g_last_error[512] = "";
 
@@ -19,6 +24,13 @@ void set_error(const char* fmt, ...) {
 extern "C" const char* esgd_last_error(void) { return esgd::g_last_error; }
 
 extern "C" int esgd_abi_version(void) { return 1; }
+
+extern "C" int esgd_set_sm_reserve(int32_t sms) {
+  ESGD_REQUIRE(sms >= 0 && sms <= esgd::kNumSMs - 16, ESGD_ERR_INPUT, "set_sm_reserve: 0..%d SMs, got %d",
+               esgd::kNumSMs - 16, sms);
+  esgd::g_sm_reserve.store(sms & ~1, std::memory_order_relaxed);  // (even: CTA pairs keep whole TPCs)
+  return ESGD_OK;
+}
 
 extern "C" int esgd_device_ok(int device) {
   cudaDeviceProp prop;

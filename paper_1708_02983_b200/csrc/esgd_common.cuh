@@ -37,6 +37,11 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 constexpr int kNumSMs = 148;
 
+// SMs the persistent tensor-core kernels leave free for a concurrently
+// running collective (esgd_set_sm_reserve; 0 by default). Only the grid size
+// changes — tile plans and split-K counts use kNumSMs, so results do not.
+int sm_reserve();
+
 // Grid for a grid-stride elementwise kernel over `work` items: enough CTAs for
 // `per_sm` resident blocks on each of the 148 SMs, never more than the work.
 inline int stride_grid(int64_t work, int threads, int per_sm = 8) {

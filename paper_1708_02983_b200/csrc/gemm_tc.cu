@@ -1370,7 +1370,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
   // CTA pairs in PAIR mode: clusters of 2 on one TPC)
   const int64_t units = (int64_t)tiles * splits;
   if (PAIR) {
-    const int pairs = (int)std::min<int64_t>(units, kNumSMs / 2);
+    const int pairs = (int)std::min<int64_t>(units, (kNumSMs - sm_reserve()) / 2);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(2 * pairs);
@@ -1387,7 +1387,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
     e = cudaLaunchKernelEx(&cfg, k_tc_gemm<BN, SPLIT, AMN, BMN, true, GM>, ma, mb, mc, ep, ga);
     ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "tc_gemm: cluster launch: %s", cudaGetErrorString(e));
   } else {
-    const int grid = (int)std::min<int64_t>(units, kNumSMs);
+    const int grid = (int)std::min<int64_t>(units, kNumSMs - sm_reserve());
     k_tc_gemm<BN, SPLIT, AMN, BMN, false, GM><<<grid, cta_threads(BN, SPLIT), C::kSmemBytes, st>>>(ma, mb, mc, ep, ga);
   }
   if (splits > 1) {

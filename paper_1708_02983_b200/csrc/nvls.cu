@@ -227,6 +227,43 @@ extern "C" int esgd_sync_update_nvls_f32(float* W, int64_t ldw, const float* G, 
   return check_launch("esgd_sync_update_nvls_f32");
 }
 
+// Dedicated-SM variant (ctas < 0 in esgd_center_step_nvls_f32): -ctas CTAs
+// of 512 threads, four float4 NVLS loads in flight per thread, each CTA
+// asking for 16 KB of (unused) shared memory so that it cannot share an SM
+// with a persistent GEMM CTA: the GEMMs run on the other SMs
+// (esgd_set_sm_reserve) instead of being slowed where a center CTA sits next
+// to one (a co-resident center CTA slows its SM's GEMM CTA, and with static
+// tile assignment the whole GEMM waits for that SM).
+__global__ void __launch_bounds__(512) k_center_nvls_wide(const float* __restrict__ C_old, const float* S_mc,
+                                                          float* C_new_mc, int64_t lo, int64_t hi, float er,
+                                                          float p) {
+  constexpr int U = 4;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = lo + tid; i0 < hi; i0 += U * nth) {
+    float4 s[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * nth;
+      if (i < hi) {
+        s[u] = mc_ld_reduce4(S_mc + 4 * i);
+        c[u] = ld4(C_old + 4 * i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * nth;
+      if (i < hi) {
+        float4 o;
+        o.x = center_rule(c[u].x, s[u].x, p, er);
+        o.y = center_rule(c[u].y, s[u].y, p, er);
+        o.z = center_rule(c[u].z, s[u].z, p, er);
+        o.w = center_rule(c[u].w, s[u].w, p, er);
+        mc_st4(C_new_mc + 4 * i, o);
+      }
+    }
+  }
+}
+
 extern "C" int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, float* C_new_mc, int64_t n4,
                                          int32_t world, int32_t rank, float etarho, int32_t num_workers,
                                          int32_t ctas, esgd_stream_t stream) {
@@ -238,6 +275,12 @@ extern "C" int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, 
                ESGD_ERR_INPUT, "center_step_nvls: null or misaligned pointer");
   const int64_t nv = n4 / 4, per = (nv + world - 1) / world;
   const int64_t lo = std::min<int64_t>(nv, per * rank), hi = std::min<int64_t>(nv, lo + per);
+  if (ctas < 0) {  // dedicated SMs
+    k_center_nvls_wide<<<-ctas, 512, 16384, reinterpret_cast<cudaStream_t>(stream)>>>(C_old, S_mc, C_new_mc, lo,
+                                                                                      hi, etarho,
+                                                                                      (float)num_workers);
+    return check_launch("esgd_center_step_nvls_f32");
+  }
   const int grid = ctas > 0 ? ctas : kNumSMs;
   k_center_nvls<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(C_old, S_mc, C_new_mc, lo, hi, etarho,
                                                                           (float)num_workers);

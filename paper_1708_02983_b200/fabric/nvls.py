@@ -27,6 +27,21 @@ def nvls_wanted() -> bool:
     return os.environ.get("ESGD_NVLS", "1") != "0"
 
 
+def nvls_reserve_sms() -> int:
+    """SMs the overlapped center kernel takes for itself while the GEMMs use
+    the rest (ESGD_NVLS_RESERVE; default 0 = small center CTAs on every SM,
+    co-resident with the GEMM CTAs). Measured at N = 2 (AlexNet, B200): 8
+    reserved SMs make the round 10% slower (4.84 -> 5.34 ms): the GEMMs on 140
+    SMs lose more than the 5% of SMs (whole extra waves of tiles) and the
+    center on 8 SMs takes 1.4 ms instead of 0.7 (tools/nvls_timeline.py)."""
+    return int(os.environ.get("ESGD_NVLS_RESERVE", "0"))
+
+
+def nvls_center_ctas() -> int:
+    r = nvls_reserve_sms()
+    return -r if r > 0 else int(os.environ.get("ESGD_NVLS_CTAS", "148"))
+
+
 def nvls_fused_single_kernel() -> bool:
     """ESGD_NVLS=fused: center + workers in one kernel after the backward
     (measured slower than the default split, which overlaps the center's
@@ -77,8 +92,8 @@ class NvlsRound:
         of C[p^1] = center step of C[p] with the all-rank sum of S[p]
         (NVSwitch ld_reduce), broadcast to every rank (multicast store)."""
         p = parity & 1
-        if ctas is None:  # one small CTA per SM, co-resident with the GEMM CTAs
-            ctas = int(os.environ.get("ESGD_NVLS_CTAS", "148"))
+        if ctas is None:
+            ctas = nvls_center_ctas()
         self.barrier(stream)
         _lib.call("esgd_center_step_nvls_f32", self.C[p].data_ptr(), self.S_mc[p], self.C_mc[p ^ 1], self.ld,
                   self.world, self.rank, hyper.etarho32, int(num_workers), ctas, stream_ptr(stream))

@@ -32,10 +32,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .. import _lib
 from ..device import require_cuda, round_up, stream_ptr
 from ..errors import InputError
 from ..fabric.collectives import CabiComm, allreduce_sum_, local_workers, replica_sum_, world
-from ..fabric.nvls import NvlsRound, nvls_fused_single_kernel, nvls_wanted
+from ..fabric.nvls import NvlsRound, nvls_fused_single_kernel, nvls_reserve_sms, nvls_wanted
 from ..fabric.engine import CATEGORIES
 from ..rng import stream_seed
 from ..updates import sync_update_, sync_update_solo_, sync_update_sum_
@@ -156,7 +157,18 @@ class SyncEngine:
             allreduce_sum_(self.S)  # torch.distributed, on the current stream
 
     def _gradient(self, stream) -> None:
-        self.plan.gradient(self.G, self.W, stream_ptr(stream))
+        # NVLS overlap: the center kernel takes `reserve` whole SMs, the
+        # forward/backward's persistent GEMMs the others (their grids are
+        # fixed at launch / graph capture; results do not depend on them)
+        reserve = (nvls_reserve_sms() if self.nvls is not None and self.overlap and not self.nvls_single
+                   and not self._nocomm and not self.solo else 0)
+        if reserve:
+            _lib.call("esgd_set_sm_reserve", reserve)
+        try:
+            self.plan.gradient(self.G, self.W, stream_ptr(stream))
+        finally:
+            if reserve:
+                _lib.call("esgd_set_sm_reserve", 0)
 
     def _update(self, stream) -> None:
         if self._nocomm:  # timing twin without the cross-GPU part: the local fused update only
