@@ -116,6 +116,13 @@ int esgd_sync_update_nvls_f32(float* W, int64_t ldw, const float* G, int64_t ldg
 int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, float* C_new_mc, int64_t n4,
                               int32_t world, int32_t rank, float etarho, int32_t num_workers, int32_t ctas,
                               esgd_stream_t stream);
+/* Copy-engine variant of the center slice: C_new = center step of C_old with
+ * sum(srcs[0..nsrc)) (device array of nsrc <= 8 slice pointers, summed in
+ * binomial order), all over n4 floats; the slices are moved between GPUs by
+ * esgd_copy_async (cudaMemcpyAsync: copy engines over NVLink).              */
+int esgd_center_step_sum_f32(const float* C_old, const float* const* srcs, int32_t nsrc, float* C_new,
+                             int64_t n4, float etarho, int32_t num_workers, esgd_stream_t stream);
+int esgd_copy_async(void* dst, const void* src, int64_t bytes, esgd_stream_t stream);
 int esgd_worker_step_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
                              const float* C, float* S_next, int64_t n4, float eta, float etarho,
                              esgd_stream_t stream);

@@ -121,6 +121,8 @@ _SIGS = {
     "esgd_tc_conv_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
     "esgd_tc_conv_tma_f32": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(ConvGather), i32, vp]),
     "esgd_set_sm_reserve": (C.c_int, [i32]),
+    "esgd_center_step_sum_f32": (C.c_int, [vp, vp, i32, vp, i64, f32, i32, vp]),
+    "esgd_copy_async": (C.c_int, [vp, vp, i64, vp]),
     "esgd_tc_conv_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_tc_gemm_ws_floats": (C.c_int, [C.POINTER(TcGemmDesc), C.POINTER(i64)]),
     "esgd_act_fwd_f32": (C.c_int, [vp, vp, i64, i32, vp]),

@@ -287,6 +287,60 @@ extern "C" int esgd_center_step_nvls_f32(const float* C_old, const float* S_mc, 
   return check_launch("esgd_center_step_nvls_f32");
 }
 
+// Copy-engine variant of the center slice (ESGD_NVLS=ce): the ranks' slices
+// of S arrive in local buffers through cudaMemcpyAsync over NVLink (copy
+// engines: no SM time taken from the forward / backward running beside it),
+// are summed here in binomial rank order, and the center step is applied;
+// the caller then copies the new slice to every peer.
+__global__ void __launch_bounds__(256) k_center_sum(const float* __restrict__ C_old,
+                                                    const float* const* __restrict__ src, int nsrc,
+                                                    float* __restrict__ C_new, int64_t nv, float er, float p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    float vx[8], vy[8], vz[8], vw[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < nsrc) {
+        const float4 v = ld4(src[r] + 4 * i);
+        vx[r] = v.x; vy[r] = v.y; vz[r] = v.z; vw[r] = v.w;
+      } else {
+        vx[r] = vy[r] = vz[r] = vw[r] = 0.f;
+      }
+    }
+    const float4 c = ld4(C_old + 4 * i);
+    float4 o;
+    o.x = center_rule(c.x, binomial_sum<8>(vx, nsrc), p, er);
+    o.y = center_rule(c.y, binomial_sum<8>(vy, nsrc), p, er);
+    o.z = center_rule(c.z, binomial_sum<8>(vz, nsrc), p, er);
+    o.w = center_rule(c.w, binomial_sum<8>(vw, nsrc), p, er);
+    st4(C_new + 4 * i, o);
+  }
+}
+
+extern "C" int esgd_center_step_sum_f32(const float* C_old, const float* const* srcs, int32_t nsrc, float* C_new,
+                                        int64_t n4, float etarho, int32_t num_workers, esgd_stream_t stream) {
+  ESGD_REQUIRE(n4 >= 0 && (n4 & 3) == 0, ESGD_ERR_SHAPE, "center_step_sum: length must be a multiple of 4");
+  ESGD_REQUIRE(nsrc >= 1 && nsrc <= 8 && num_workers >= 1, ESGD_ERR_INPUT, "center_step_sum: 1..8 sources");
+  if (n4 == 0) return ESGD_OK;
+  ESGD_REQUIRE(C_old && srcs && C_new && aligned16(C_old) && aligned16(C_new), ESGD_ERR_INPUT,
+               "center_step_sum: null or misaligned pointer");
+  const int64_t nv = n4 / 4;
+  k_center_sum<<<stride_grid(nv, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      C_old, srcs, nsrc, C_new, nv, etarho, (float)num_workers);
+  return check_launch("esgd_center_step_sum_f32");
+}
+
+// stream-ordered device copy (peer pointers of symmetric memory included):
+// the copy engines move the CE variant's slices
+extern "C" int esgd_copy_async(void* dst, const void* src, int64_t bytes, esgd_stream_t stream) {
+  ESGD_REQUIRE(bytes >= 0, ESGD_ERR_SHAPE, "copy_async: negative size");
+  if (bytes == 0) return ESGD_OK;
+  ESGD_REQUIRE(dst && src, ESGD_ERR_INPUT, "copy_async: null pointer");
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  ESGD_REQUIRE(e == cudaSuccess, ESGD_ERR_CUDA, "copy_async: %s", cudaGetErrorString(e));
+  return ESGD_OK;
+}
+
 extern "C" int esgd_worker_step_sum_f32(float* W, int64_t ldw, const float* G, int64_t ldg, int32_t nrep,
                                         const float* C, float* S_next, int64_t n4, float eta, float etarho,
                                         esgd_stream_t stream) {

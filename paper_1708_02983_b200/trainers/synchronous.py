@@ -126,7 +126,7 @@ class SyncEngine:
         self.graphs = [None, None]
         self._nocomm = False
         self.nvls_single = nvls_fused_single_kernel()
-        self.collective = ("nvls-fused" if self.nvls is not None else
+        self.collective = (("nvls-ce" if self.nvls.ce else "nvls-fused") if self.nvls is not None else
                            ("nccl-cabi" if self.cabi is not None else
                             ("nccl-allreduce" if self.world > 1 else "none")))
 
