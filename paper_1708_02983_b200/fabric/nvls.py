@@ -62,7 +62,7 @@ class NvlsRound:
     """Symmetric S/C buffers, their multicast addresses and the barrier flags
     of one rank; ``update(...)`` enqueues barrier + fused update for a round."""
 
-    def __init__(self, ld: int, device, group=None):
+    def __init__(self, ld: int, device, group=None, nrep: int = 0):
         import torch.distributed._symmetric_memory as symm
 
         if ld % 4:
@@ -71,7 +71,11 @@ class NvlsRound:
         gname = group.group_name
         self.ld = ld
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
-        self.buf = symm.empty(4 * ld, dtype=torch.float32, device=device)
+        # copy-engine path with one worker per rank: the worker buffer W itself
+        # lives in the symmetric allocation too (after S[0], S[1], C[0], C[1]),
+        # its peers read their slice of it directly — no local sum S to form
+        self.w_src = nvls_copy_engines() and nrep == 1
+        self.buf = symm.empty((5 if self.w_src else 4) * ld, dtype=torch.float32, device=device)
         self.buf.zero_()
         self.h = symm.rendezvous(self.buf, gname)
         if not self.h.multicast_ptr:
@@ -91,6 +95,7 @@ class NvlsRound:
         self.C = [self.buf[2 * ld:3 * ld], self.buf[3 * ld:4 * ld]]
         self.S_mc = [self.mc, self.mc + 4 * ld]
         self.C_mc = [self.mc + 8 * ld, self.mc + 12 * ld]
+        self.W = self.buf[4 * ld:5 * ld].view(1, ld) if self.w_src else None
         # copy-engine variant: this rank's slice [lo, hi) (floats, multiple of
         # 4) of every rank's S lands in recv[j]; peers' buffers by address
         self.ce = nvls_copy_engines()
@@ -103,8 +108,8 @@ class NvlsRound:
             self.recv = torch.empty((self.world, max(4, self.hi - self.lo)), dtype=torch.float32, device=device)
             srcs = []
             for q in range(2):
-                srcs.append([self.S[q].data_ptr() + 4 * self.lo if j == self.rank else self.recv[j].data_ptr()
-                             for j in range(self.world)])
+                own = (self.W if self.w_src else self.S[q]).data_ptr() + 4 * self.lo
+                srcs.append([own if j == self.rank else self.recv[j].data_ptr() for j in range(self.world)])
             self.srcs = torch.tensor(srcs, dtype=torch.int64, device=device)
 
     def barrier(self, stream=None) -> None:
@@ -127,17 +132,22 @@ class NvlsRound:
 
     def center_ce(self, p: int, num_workers: int, hyper, stream=None) -> None:
         """Copy-engine center slice of round parity p: barrier; pull this
-        rank's slice of every peer's S[p] (cudaMemcpyAsync over NVLink); sum in
-        rank order + center step into C[p^1]'s slice; push it to every peer."""
+        rank's slice of every peer's S[p] (or, one worker per rank, of its W:
+        then a second barrier, after which the ranks' worker steps may
+        overwrite W) with cudaMemcpyAsync over NVLink; sum in rank order +
+        center step into C[p^1]'s slice; push it to every peer."""
         self.barrier(stream)
         n = self.hi - self.lo
+        sp = stream_ptr(stream)
+        s_off = 4 * ((4 if self.w_src else p) * self.ld + self.lo)
+        c_off = 4 * ((2 + (p ^ 1)) * self.ld + self.lo)
+        for j in range(self.world):
+            if j != self.rank and n > 0:
+                _lib.call("esgd_copy_async", self.recv[j].data_ptr(), self.peer[j] + s_off, 4 * n, sp)
+        if self.w_src:
+            self.barrier(stream)
         if n <= 0:
             return
-        sp = stream_ptr(stream)
-        s_off, c_off = 4 * (p * self.ld + self.lo), 4 * ((2 + (p ^ 1)) * self.ld + self.lo)
-        for j in range(self.world):
-            if j != self.rank:
-                _lib.call("esgd_copy_async", self.recv[j].data_ptr(), self.peer[j] + s_off, 4 * n, sp)
         _lib.call("esgd_center_step_sum_f32", self.C[p].data_ptr() + 4 * self.lo, self.srcs[p].data_ptr(),
                   self.world, self.C[p ^ 1].data_ptr() + 4 * self.lo, n, hyper.etarho32, int(num_workers), sp)
         for j in range(self.world):
@@ -145,8 +155,14 @@ class NvlsRound:
                 _lib.call("esgd_copy_async", self.peer[j] + c_off, self.C[p ^ 1].data_ptr() + 4 * self.lo, 4 * n, sp)
 
     def workers(self, W: torch.Tensor, G: torch.Tensor, parity: int, hyper, stream=None) -> None:
-        """Local half: worker step against C[p], S[p^1] = replica sum of the new W."""
+        """Local half: worker step against C[p], S[p^1] = replica sum of the new
+        W (one worker per rank on the copy-engine path: the worker step alone,
+        16 B/param, in place on the symmetric W)."""
         p = parity & 1
+        if self.w_src:
+            _lib.call("esgd_worker_step_f32", W.data_ptr(), W.data_ptr(), G.data_ptr(), self.C[p].data_ptr(),
+                      self.ld, hyper.eta32, hyper.etarho32, stream_ptr(stream))
+            return
         _lib.call("esgd_worker_step_sum_f32", W.data_ptr(), W.stride(0), G.data_ptr(), G.stride(0), W.shape[0],
                   self.C[p].data_ptr(), self.S[p ^ 1].data_ptr(), self.ld, hyper.eta32, hyper.etarho32,
                   stream_ptr(stream))

@@ -106,7 +106,7 @@ class SyncEngine:
             torch.cuda.synchronize()
             if self.fused_sum and nvls_wanted():
                 try:
-                    self.nvls = NvlsRound(ld, dev)
+                    self.nvls = NvlsRound(ld, dev, nrep=self.nrep)
                 except Exception as exc:  # no multicast object support: NCCL path
                     warnings.warn(f"NVLS multicast unavailable ({exc}); using one NCCL allreduce per round",
                                   RuntimeWarning, stacklevel=2)
@@ -116,6 +116,9 @@ class SyncEngine:
                 self.nvls.C[0].copy_(self.C)
                 self.nvls.S[0].copy_(self.S)
                 self.C, self.S = self.nvls.C[0], self.nvls.S[0]
+                if self.nvls.w_src:  # peers read this rank's W in place
+                    self.nvls.W.copy_(self.W)
+                    self.W = self.nvls.W
                 torch.cuda.synchronize()
         # ESGD_COLLECTIVE=cabi: the allreduce through libesgd's own NCCL
         # communicator (the C-ABI path of hosts without torch.distributed)
@@ -172,7 +175,9 @@ class SyncEngine:
 
     def _update(self, stream) -> None:
         if self._nocomm:  # timing twin without the cross-GPU part: the local fused update only
-            if self.solo:
+            if self.nvls is not None and self.nvls.w_src:
+                self.nvls.workers(self.W, self.G, self.parity, self.cfg.hyper, stream)
+            elif self.solo:
                 sync_update_solo_(self.W, self.G, self.C, self.n, self.cfg.hyper, stream)
             else:
                 sync_update_sum_(self.W, self.G, self.C, self.S, self.S, self.n, self.P, self.cfg.hyper, stream)

@@ -4,7 +4,7 @@ round with ESGD_NVLS=0; CUDA-graph captured) must equal the
 single-process run bitwise for N = 2 (a two-term sum is order-free) and
 within 1e-6 relative otherwise.
 
-    torchrun --nproc-per-node N tools/dist_check.py
+    torchrun --nproc-per-node N tools/dist_check.py     # DIST_PER_RANK=1: one worker per rank
 """
 import os
 import sys
@@ -27,7 +27,7 @@ def main():
     world, rank = dist.get_world_size(), dist.get_rank()
     train = normalize(gen_synthetic(10, 784, 200, seed=0, separation=5.0))
     prob = NetworkProblem(network.lenet(seed=0), train)
-    P = 2 * world
+    P = int(os.environ.get("DIST_PER_RANK", "2")) * world
     # N > 2: the switch / ring sum order differs from the binomial tree, and a
     # randomly initialised LeNet amplifies last-bit differences over rounds,
     # so fewer rounds there (the tolerance is the north-star 1e-5)
