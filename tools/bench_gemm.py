@@ -50,7 +50,7 @@ def run(name, m, n, k, am, bm, cm, precision, reps=10):
     A = torch.randn((kp * mp,), device="cuda")
     B = torch.randn((kp * np_,), device="cuda")
     Cm = torch.empty((m * n,), device="cuda")
-    ws = torch.empty(1 << 24, device="cuda")
+    ws = torch.zeros(1 << 24, device="cuda")  # (split-K tile counters start at zero)
     lda = mp if am else kp
     ldb = np_ if bm else kp
     c_sm, c_sn = (1, mp) if cm else (np_, 1)

@@ -54,7 +54,7 @@ def main():
         from paper_1708_02983_b200.device import stream_ptr
         import ctypes as C
         co = torch.empty(m, n, device="cuda")
-        ws = torch.empty(1 << 24, device="cuda")
+        ws = torch.zeros(1 << 24, device="cuda")  # (split-K tile counters start at zero)
         if k % 4 == 0 and n % 4 == 0:
             d = _lib.TcGemmDesc(m, n, k, 1, a.data_ptr(), k, 0, b.data_ptr(), n, 0, co.data_ptr(), n, 1, 0,
                                 None, 0, None, 0, 0, 0, 0, 0, 3, 0, 1, ws.data_ptr(), ws.numel())
