@@ -40,6 +40,11 @@ SHAPES = [
     ("x.conv5.fwdT", 256, 21632, 2304, 0, 1, 0),
     ("x.conv3.fwdT", 384, 21632, 1728, 0, 1, 0),
     ("x.conv2.fwdT", 192, 93312, 1600, 0, 1, 0),
+    # conv1 with a K-major (pixel-row) im2col matrix: forward A K-major, wgrad B MN-major
+    ("x.conv1.fwd.kmajor", 387200, 64, 363, 0, 0, 1),
+    ("x.conv1.wgrad.bmn", 64, 363, 387200, 0, 1, 0),
+    ("x.conv2.fwd.kmajor", 93312, 192, 1600, 0, 0, 1),
+    ("x.conv2.wgrad.bmn", 192, 1600, 93312, 0, 1, 0),
 ]
 
 
