@@ -1221,10 +1221,10 @@ int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64
 
 // N tile width. 192-wide tiles (3 smem stages, 2 TMEM A slots) read the
 // TS-mode A operand from TMEM once per 192 instead of 128 output columns, so
-// they win wherever they do not add padding and there are enough M tiles to
+// they win wherever they add little padding and there are enough M tiles to
 // fill the SMs (measured: conv2 fwd N=192 0.34 -> 0.25 ms, conv3 fwd N=384
-// 0.154 -> 0.143, conv4 dgrad N=3456 0.201 -> 0.189); with more padding
-// (N = 1600) or a single M tile (the FC layers, M = batch) 128 stays faster.
+// 0.154 -> 0.143, conv4 dgrad N=3456 0.201 -> 0.189); with a single M tile
+// (the FC layers, M = batch) 128 stays faster.
 inline int64_t padded(int64_t n, int bn) { return ((n + bn - 1) / bn) * bn; }
 inline int pick_bn(int64_t m, int64_t n, bool split) {
   static const int force = getenv("ESGD_TC_BN") ? atoi(getenv("ESGD_TC_BN")) : 0;  // tuning runs
@@ -1232,7 +1232,11 @@ inline int pick_bn(int64_t m, int64_t n, bool split) {
   if (n <= 64) return 64;
   if (!split) return 128;
   if (padded(n, 192) < padded(n, 128)) return 192;
-  return (padded(n, 192) == padded(n, 128) && m >= 16 * BM) ? 192 : 128;
+  // with >= 16 M tiles 192 also wins at up to ~4% more padding: conv2's data
+  // gradient (N = 1600: 1728 vs 1664 columns) 0.338 -> 0.318 ms, because A is
+  // loaded and split once per 192 instead of 128 output columns (the FC weight
+  // gradients at N = 4096 are neutral)
+  return (padded(n, 192) * 100 <= padded(n, 128) * 104 && m >= 16 * BM) ? 192 : 128;
 }
 // CTA-pair mode (cta_group::2, 256-row units) for the 3xTF32 path when M has
 // enough rows that 256-row tiles add little padding (ESGD_TC_PAIR=0/1 forces

@@ -28,6 +28,7 @@ SHAPES = [
     ("fc6.fwd", 128, 4096, 9216, 0, 1, 0),
     ("fc6.wgrad", 9216, 4096, 128, 1, 0, 0),
     ("fc6.dgrad", 128, 9216, 4096, 0, 0, 0),
+    ("fc7.wgrad", 4096, 4096, 128, 1, 0, 0),
     # exploration: the short-K problems with the big operand as B instead
     ("x.conv2.dgradT", 1600, 93312, 192, 0, 1, 0),
     ("x.fc6.wgradT", 4096, 9216, 128, 0, 1, 1),
