@@ -435,6 +435,9 @@ def test_sync_update_sum_equals_update_then_tree_sum(nrep, n):
     (192, 1600, 4096, 0, 0, False),  # M = 192 weight gradient: swapped orientation, BN = 192, split-K
     (64, 363, 20000, 0, 0, False),   # M = 64 weight gradient: swapped orientation, split-K
     (1000, 1600, 192, 1, 0, False),  # dgrad shape class, BN = 192 with a padded last tile
+    (2048, 256, 512, 1, 0, True),    # conv4/5 forward class: swapped to N = 2048 with the bias per row
+    (3000, 64, 364, 1, 0, True),     # conv1 forward class (N = 64): swapped, bias per row, M-padded swap
+    (4000, 256, 96, 1, 0, True),     # swapped, split-free short K, bias + relu
 ])
 def test_tcgen05_gemm_wide_tiles_and_orientation(m, n, k, a_major, b_major, bias):
     """the 192-wide N tiles (TMEM A ring of 2) and the padded-work orientation
