@@ -340,7 +340,6 @@ struct Epi {
   int splits, kb_per_split, batch;
   int out_mode;     // 0 direct stores (via smem staging), 1 TMA store M-contiguous C, 2 TMA store N-contiguous C
   int m_fast;       // rasterise units m-fastest (M-contiguous output) else n-fastest
-  int bias_rows;    // bias indexed by row (the caller's per-column bias of a swapped orientation)
 };
 
 // Implicit-GEMM operand gathered by the split warps straight from a CNHW
@@ -446,8 +445,7 @@ __device__ __forceinline__ void gather_cp(const Gather& g, const float* zs, int 
 
 // epilogue value without the read-modify-write of accumulate (TMA-store path)
 __device__ __forceinline__ float epi_value(const Epi& ep, float x, int z, int row, int col) {
-  if (ep.bias && (ep.bias_rows ? row < ep.m : col < ep.n))
-    x = __fadd_rn(x, ep.bias[z * ep.bias_sb + (ep.bias_rows ? row : col)]);
+  if (ep.bias && col < ep.n) x = __fadd_rn(x, ep.bias[z * ep.bias_sb + col]);
   x = act_apply(x, ep.act);
   if (ep.mask && row < ep.m && col < ep.n)
     x = __fmul_rn(x, ep.mask[z * ep.mask_sb + (int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
@@ -459,7 +457,7 @@ __device__ __forceinline__ float epi_apply(const Epi& ep, float x, int z, int ro
   const float* bz = ep.bias ? ep.bias + z * ep.bias_sb : nullptr;
   const float* mz = ep.mask ? ep.mask + z * ep.mask_sb : nullptr;
   if (ep.accumulate) x = __fadd_rn(cz[off], x);
-  if (bz) x = __fadd_rn(x, bz[ep.bias_rows ? row : col]);
+  if (bz) x = __fadd_rn(x, bz[col]);
   x = act_apply(x, ep.act);
   if (mz) x = __fmul_rn(x, mz[(int64_t)row * ep.mask_sm + (int64_t)col * ep.mask_sn] > 0.f ? 1.f : 0.f);
   return x;
@@ -565,12 +563,10 @@ __device__ __forceinline__ uint32_t stage_addr(uint32_t sb, int r, int j) {
 }
 
 // registers -> smem for the thread's local quarter lq (columns col0..col0+31
-// of the tile row); FAST applies bias (per column from bz, or the row's rb
-// when use_rb) + identity/relu
+// of the tile row); FAST applies bias + identity/relu
 template <int NACC, int MODE, bool FAST>
 __device__ __forceinline__ void stage_quarter(const float (&racc)[NACC], int lq, uint32_t sb, int r,
-                                              const float* bz, bool relu, int col0, int n, float rb,
-                                              bool use_rb) {
+                                              const float* bz, bool relu, int col0, int n) {
 #pragma unroll
   for (int jj = 0; jj < 32; jj += 4) {
     const int j = lq * 32 + jj;
@@ -580,7 +576,6 @@ __device__ __forceinline__ void stage_quarter(const float (&racc)[NACC], int lq,
       float x = racc[j + e];
       if (FAST) {
         if (bz) x = __fadd_rn(x, col0 + jj + e < n ? __ldg(bz + col0 + jj + e) : 0.f);
-        else if (use_rb) x = __fadd_rn(x, rb);
         if (relu) x = fmaxf(x, 0.f);
       }
       v[e] = x;
@@ -1078,9 +1073,6 @@ __global__ void __launch_bounds__(cta_threads(BN, SPLIT), 1)
                           ep.out_mode != 0;
         const bool relu = ep.act == ESGD_ACT_RELU;
         const float* bz = ep.bias ? ep.bias + w.z * ep.bias_sb : nullptr;
-        const bool use_rb = bz && ep.bias_rows;
-        const float rb = (use_rb && row < ep.m) ? __ldg(bz + row) : 0.f;
-        if (use_rb) bz = nullptr;
         const int r = q * 32 + lane;
 #pragma unroll
         for (int lq = 0; lq < HB / 32; ++lq) {
@@ -1089,11 +1081,11 @@ __global__ void __launch_bounds__(cta_threads(BN, SPLIT), 1)
           if (threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           named_bar_sync(1 + h, 128);
           if (ep.out_mode == 2) {
-            if (fast) stage_quarter<HB, 2, true>(racc, lq, sb, r, bz, relu, col0, ep.n, rb, use_rb);
-            else stage_quarter<HB, 2, false>(racc, lq, sb, r, bz, relu, col0, ep.n, rb, use_rb);
+            if (fast) stage_quarter<HB, 2, true>(racc, lq, sb, r, bz, relu, col0, ep.n);
+            else stage_quarter<HB, 2, false>(racc, lq, sb, r, bz, relu, col0, ep.n);
           } else {
-            if (fast) stage_quarter<HB, 1, true>(racc, lq, sb, r, bz, relu, col0, ep.n, rb, use_rb);
-            else stage_quarter<HB, 1, false>(racc, lq, sb, r, bz, relu, col0, ep.n, rb, use_rb);
+            if (fast) stage_quarter<HB, 1, true>(racc, lq, sb, r, bz, relu, col0, ep.n);
+            else stage_quarter<HB, 1, false>(racc, lq, sb, r, bz, relu, col0, ep.n);
           }
           if (!fast) general_quarter(ep, sb, r, row, w.z, col0);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1227,51 +1219,37 @@ int make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64
   return ESGD_OK;
 }
 
-// Tile plan cost model (3xTF32). Measured on the AlexNet shapes
-// (tools/sweep_gemm.sh, orientation x tile width x CTA pairs): per useful
-// output column a 192-wide tile is the cheapest — A is loaded and split once
-// per 192 columns and a 128 x 192 x 8 MMA does not cost 1.5x a 128 x 128 x 8
-// one — a 128-wide tile costs ~1.3x and a 64-wide one ~2.2x (a 128 x 64 x 8
-// MMA takes ~45 cycles, not 32). So: pick the width minimising padded columns
-// x that factor, and the orientation (C^T = B.A^T) minimising padded area x
-// factor, swapping only for a >= 5% gain (conv4/5's forward, N = 256: swapped
-// to N = 21632 at 192 wide, 0.247 -> 0.180 ms; conv1's forward, N = 64, and
-// conv2's weight gradient swap too; conv2's data gradient, conv3's forward,
-// the FC layers do not). Before round 2's sweep the rule only minimised
-// padding, which left conv3-5's forwards at 128-wide tiles.
+// N tile width. 192-wide tiles (3 smem stages, 2 TMEM A slots) read the
+// TS-mode A operand from TMEM once per 192 instead of 128 output columns, so
+// they win wherever they add little padding and there are enough M tiles to
+// fill the SMs (measured: conv2 fwd N=192 0.34 -> 0.25 ms, conv3 fwd N=384
+// 0.154 -> 0.143, conv4 dgrad N=3456 0.201 -> 0.189); with a single M tile
+// (the FC layers, M = batch) 128 stays faster.
 inline int64_t padded(int64_t n, int bn) { return ((n + bn - 1) / bn) * bn; }
-inline double bn_factor(int bn) { return bn == 64 ? 2.2 : bn == 128 ? 1.3 : 1.0; }
 inline int pick_bn(int64_t m, int64_t n, bool split) {
   static const int force = getenv("ESGD_TC_BN") ? atoi(getenv("ESGD_TC_BN")) : 0;  // tuning runs
   if (force == 64 || force == 128 || (force == 192 && split)) return force;
-  (void)m;
-  if (!split) return n <= 64 ? 64 : 128;
-  int best = 192;
-  double cost = (double)padded(n, 192);
-  const int cands[2] = {128, 64};
-  for (int bn : cands) {
-    if (bn == 64 && n > 64) continue;
-    const double c = (double)padded(n, bn) * bn_factor(bn);
-    if (c < cost) { cost = c; best = bn; }
-  }
-  return best;
+  if (n <= 64) return 64;
+  if (!split) return 128;
+  if (padded(n, 192) < padded(n, 128)) return 192;
+  // with >= 16 M tiles 192 also wins at up to ~4% more padding: conv2's data
+  // gradient (N = 1600: 1728 vs 1664 columns) 0.338 -> 0.318 ms, because A is
+  // loaded and split once per 192 instead of 128 output columns (the FC weight
+  // gradients at N = 4096 are neutral)
+  return (padded(n, 192) * 100 <= padded(n, 128) * 104 && m >= 16 * BM) ? 192 : 128;
 }
 // CTA-pair mode (cta_group::2, 256-row units) for the 3xTF32 path when M has
-// at least one full pair tile and 256-row tiles add little padding (measured:
-// even a single 256-row tile — conv4/5's swapped forward — gains from the
-// halved per-SM B traffic); ESGD_TC_PAIR=0/1 forces it off / on for tuning
+// enough rows that 256-row tiles add little padding (ESGD_TC_PAIR=0/1 forces
+// it off / on for tuning runs)
 inline bool use_pair(int64_t m, bool split) {
   static const int force = getenv("ESGD_TC_PAIR") ? atoi(getenv("ESGD_TC_PAIR")) : -1;
   if (!split || m <= BM) return false;
   if (force >= 0) return force == 1;
-  return m >= 2 * BM && padded(m, 256) * 8 <= padded(m, BM) * 9;
+  return m >= 8 * 256 && padded(m, 256) * 8 <= padded(m, BM) * 9;
 }
-// cost of an orientation: padded MMA area (M tiled by 128 or 256) x the
-// chosen width's per-column factor
-inline double padded_cost(int64_t m, int64_t n, bool split) {
-  const int bn = pick_bn(m, n, split);
-  return (double)padded(m, use_pair(m, split) ? 2 * BM : BM) * (double)padded(n, bn) *
-         (split ? bn_factor(bn) : 1.0);
+// padded MMA area of an orientation (M tiled by 128 or 256, N by the chosen width)
+inline int64_t padded_cost(int64_t m, int64_t n, bool split) {
+  return padded(m, use_pair(m, split) ? 2 * BM : BM) * padded(n, pick_bn(m, n, split));
 }
 
 // Launch plan of one GEMM: orientation (C^T = B.A^T when it needs less padded
@@ -1280,7 +1258,6 @@ struct Plan {
   esgd_tc_gemm_desc d;  // the oriented problem
   int bn, splits, kbps;
   bool pair;            // cta_group::2, 256-row units
-  bool bias_rows = false;  // swapped with a bias: the caller's columns are our rows
 };
 
 inline Plan make_plan(const esgd_tc_gemm_desc* d0, bool allow_swap = true) {
@@ -1288,23 +1265,13 @@ inline Plan make_plan(const esgd_tc_gemm_desc* d0, bool allow_swap = true) {
   p.d = *d0;
   const bool split = d0->precision == 3;
   // Orientation: C^T = B . A^T is the same GEMM with the operands' roles
-  // swapped; take it when the cost model above says so (a per-column bias
-  // then becomes a per-row one: Epi::bias_rows).
+  // swapped; take it when it needs less padded tensor-core work (M is tiled
+  // by 128: a 64- or 192-row M wastes half / a quarter of every MMA). Only
+  // without a per-column bias (the epilogue applies bias along N).
   static const int force_swap = getenv("ESGD_TC_SWAP") ? atoi(getenv("ESGD_TC_SWAP")) : -1;  // tuning runs
-  bool swap = force_swap >= 0 ? force_swap == 1
-                              : padded_cost(d0->n, d0->m, split) < 0.95 * padded_cost(d0->m, d0->n, split);
-  int force_bn = 0, force_pair = -1;
-  if (const char* e = getenv("ESGD_TC_SWAP_SHAPE")) {  // tuning runs: "MxNxK[:bn:pair]" forced swapped
-    char buf[64];
-    snprintf(buf, sizeof(buf), "%dx%dx%d", d0->m, d0->n, d0->k);
-    if (const char* hit = strstr(e, buf)) {
-      swap = true;
-      hit += strlen(buf);
-      if (*hit == ':') sscanf(hit, ":%d:%d", &force_bn, &force_pair);
-    }
-  }
-  if (allow_swap && swap) {
-    p.bias_rows = d0->bias != nullptr;
+  const bool swap = force_swap >= 0 ? force_swap == 1
+                                    : padded_cost(d0->n, d0->m, split) < padded_cost(d0->m, d0->n, split);
+  if (allow_swap && !d0->bias && swap) {
     esgd_tc_gemm_desc& sw = p.d;
     sw.m = d0->n; sw.n = d0->m;
     sw.a = d0->b; sw.lda = d0->ldb; sw.a_sb = d0->b_sb; sw.a_major = d0->b_major;
@@ -1313,8 +1280,8 @@ inline Plan make_plan(const esgd_tc_gemm_desc* d0, bool allow_swap = true) {
     sw.mask_sm = d0->mask_sn; sw.mask_sn = d0->mask_sm;
   }
   const esgd_tc_gemm_desc* d = &p.d;
-  p.bn = force_bn ? force_bn : pick_bn(d->m, d->n, split);
-  p.pair = force_pair >= 0 ? (force_pair == 1 && split && d->m > BM) : use_pair(d->m, split);
+  p.bn = pick_bn(d->m, d->n, split);
+  p.pair = use_pair(d->m, split);
   const int bmu = p.pair ? 2 * BM : BM, units_per_wave = p.pair ? kNumSMs / 2 : kNumSMs;
   const int nkb = (d->k + BK - 1) / BK;
   // The K split depends on the per-replica problem only, never on `batch` or
@@ -1405,7 +1372,7 @@ int launch(const Plan& p, cudaStream_t st, const Gather& ga = Gather{}) {
   const int m_fast = 0;  // (measured: m-fastest rasterisation was slower on every shape)
   Epi ep{d->c, d->c_sm, d->c_sn, d->c_sb, d->bias, d->bias_sb, d->mask, d->mask_sm, d->mask_sn,
          d->mask_sb, d->act, d->accumulate, d->m, d->n, d->k, d->ws, splits, kbps, d->batch, out_mode,
-         m_fast, p.bias_rows ? 1 : 0};
+         m_fast};
   // persistent: one CTA per SM (smem-limited), units dealt round-robin (to
   // CTA pairs in PAIR mode: clusters of 2 on one TPC)
   const int64_t units = (int64_t)tiles * splits;
