@@ -560,3 +560,25 @@ def test_tcgen05_gemm_short_k_many_n_tiles(m, n, k, batch, a_major, b_major):
     d.c = C2.data_ptr()
     _lib.check(_lib.load().esgd_tc_gemm_f32(C.byref(d), stream_ptr()))
     assert torch.equal(Cd, C2)
+
+
+@pytest.mark.parametrize("rows,cols,ld,batch", [(7, 50000, 50000, 1), (5, 4099, 4100, 2), (3, 9001, 9001, 1),
+                                                (64, 387200, 387200, 1), (2, 3, 4, 3)])
+def test_rowsum_vector_and_scalar_paths(rows, cols, ld, batch):
+    """esgd_rowsum_f32 (conv bias gradients): the 16-B-load path (ld % 4 ==
+    0, with a cols % 4 tail) and the scalar path, vs fp64, deterministic"""
+    rng = np.random.default_rng(rows * cols + ld)
+    x = np.zeros((batch, rows, ld), np.float32)
+    x[:, :, :cols] = rng.standard_normal((batch, rows, cols))
+    x[:, :, cols:] = 1e6  # padding beyond cols must not be summed
+    xd = dev(x)
+    out = torch.zeros((batch, rows), device="cuda")
+    scratch = torch.zeros(64 * rows * batch + 64, device="cuda")
+    _lib.call("esgd_rowsum_f32", out.data_ptr(), rows, xd.data_ptr(), ld, rows * ld, rows, cols, batch,
+              scratch.data_ptr(), stream_ptr())
+    ref = x[:, :, :cols].astype(np.float64).sum(axis=2)
+    assert rel_err(host(out), ref) < 1e-5
+    out2 = torch.zeros_like(out)
+    _lib.call("esgd_rowsum_f32", out2.data_ptr(), rows, xd.data_ptr(), ld, rows * ld, rows, cols, batch,
+              scratch.data_ptr(), stream_ptr())
+    assert torch.equal(out, out2)
