@@ -79,3 +79,32 @@ def test_collective_argument_checks():
         call("esgd_nccl_init", C.byref(comm), C.cast(uid, C.c_void_p), 2, 2)
     call("esgd_nccl_destroy", NULL)  # null communicator: no-op
     assert _lib.load().esgd_nccl_available() in (0, 1)
+
+
+def test_round2_entries_validate_before_the_device():
+    """the copy-engine round pieces, the SM reserve, the TMA-im2col conv and
+    the fused-relu pool backward reject bad arguments without a launch"""
+    with pytest.raises(InputError):
+        call("esgd_copy_async", NULL, FAKE, 16, NULL)           # null destination with bytes to move
+    with pytest.raises(ShapeError):
+        call("esgd_copy_async", FAKE, FAKE, -4, NULL)
+    call("esgd_copy_async", NULL, NULL, 0, NULL)                # nothing to move: no-op
+    with pytest.raises(InputError):
+        call("esgd_center_step_sum_f32", FAKE, FAKE, 0, FAKE, 64, 0.01, 2, NULL)    # no sources
+    with pytest.raises(InputError):
+        call("esgd_center_step_sum_f32", FAKE, FAKE, 9, FAKE, 64, 0.01, 2, NULL)    # > 8 sources
+    with pytest.raises(ShapeError):
+        call("esgd_center_step_sum_f32", FAKE, FAKE, 2, FAKE, 63, 0.01, 2, NULL)    # not a multiple of 4
+    call("esgd_center_step_sum_f32", NULL, NULL, 2, NULL, 0, 0.01, 2, NULL)
+    with pytest.raises(InputError):
+        call("esgd_set_sm_reserve", -2)
+    with pytest.raises(InputError):
+        call("esgd_set_sm_reserve", 140)
+    call("esgd_set_sm_reserve", 0)
+    d = _lib.TcGemmDesc(16, 4, 27, 1, None, 0, 0, FAKE, 28, 0, FAKE, 1, 16, 0, None, 0, None, 0, 0, 0, 0, 0, 3,
+                        0, 0, None, 0)
+    g = _lib.ConvGather(FAKE, 0, 0, 0, 4, 4, 4, 4, 1, -1, -1, 1, 3, 3, 16, 3)      # 3 channels: not % 32
+    assert _lib.load().esgd_tc_conv_tma_f32(C.byref(d), C.byref(g), 1, None) != 0
+    with pytest.raises(InputError):
+        call("esgd_maxpool_bwd_relu_f32", FAKE, _lib.nchw(1, 1, 4, 4), 0, FAKE, _lib.nchw(1, 1, 2, 2), 0, FAKE,
+             NULL, 0, 2, 2, 0, 1, NULL)                           # null pooled output
