@@ -42,6 +42,9 @@ __device__ __forceinline__ float act_grad_mul(float d, float z, int act) {
 // output is skinny (weight gradients of small layers) so more CTAs share the
 // split-K reduction.
 constexpr int BK = 16;
+#ifndef ESGD_REDUCE8_MIN
+#define ESGD_REDUCE8_MIN 16
+#endif
 
 __device__ __forceinline__ float epilogue(const esgd_gemm_desc& d, float acc, int z, int gm, int gn,
                                           float* C, float* Cp, int64_t off) {
@@ -185,6 +188,42 @@ __global__ void __launch_bounds__(256) k_gemm_reduce(esgd_gemm_desc d, int split
     const int gm = (int)(e / d.n), gn = (int)(e % d.n);
     const int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
     C[off] = epilogue(d, v, z, gm, gn, C, Cp, off);
+  }
+}
+
+// Wide split-K combine: 8 threads per output element, thread j summing
+// slices j, j+8, ... (four loads in flight), then a fixed xor-shuffle tree —
+// deterministic, and the splits' loads spread over 8x more threads than
+// k_gemm_reduce (LeNet's 20 x 25 weight gradient is 128 slices deep: one
+// thread per element walked all of them)
+__global__ void __launch_bounds__(256) k_gemm_reduce8(esgd_gemm_desc d, int splits) {
+  const int64_t mn = (int64_t)d.m * d.n;
+  const int z = blockIdx.y;
+  const int sub = threadIdx.x & 7;
+  float* C = d.c + z * d.c_sb;
+  float* Cp = d.c_pre ? d.c_pre + z * d.c_sb : nullptr;
+  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  // e0 is warp-uniform (4 elements per warp), so every lane reaches the shuffles
+  for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) >> 3; e0 < mn; e0 += stride) {
+    const int64_t e = e0 + ((threadIdx.x & 31) >> 3);
+    float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+    if (e < mn) {
+      const float* P = d.ws + (int64_t)z * splits * mn + e;
+      int s = sub;
+      for (; s + 24 < splits; s += 32) {
+        v0 += P[s * mn]; v1 += P[(s + 8) * mn]; v2 += P[(s + 16) * mn]; v3 += P[(s + 24) * mn];
+      }
+      for (; s < splits; s += 8) v0 += P[s * mn];
+    }
+    float v = (v0 + v1) + (v2 + v3);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    if (sub == 0 && e < mn) {
+      const int gm = (int)(e / d.n), gn = (int)(e % d.n);
+      const int64_t off = (int64_t)gm * d.c_sm + (int64_t)gn * d.c_sn;
+      C[off] = epilogue(d, v, z, gm, gn, C, Cp, off);
+    }
   }
 }
 
@@ -411,8 +450,14 @@ extern "C" int esgd_gemm_f32(const esgd_gemm_desc* d, esgd_stream_t stream) {
   if (p.small) k_gemm<32, 32><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
   else k_gemm<64, 64><<<grid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits, kchunk);
   if (splits > 1) {
-    dim3 rgrid(stride_grid((int64_t)d->m * d->n, 256, 4), d->batch);
-    k_gemm_reduce<<<rgrid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits);
+    // deep splits over small outputs: 8 threads per element (k_gemm_reduce8)
+    if (splits >= ESGD_REDUCE8_MIN) {
+      dim3 rgrid(stride_grid((int64_t)d->m * d->n * 8, 256, 4), d->batch);
+      k_gemm_reduce8<<<rgrid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits);
+    } else {
+      dim3 rgrid(stride_grid((int64_t)d->m * d->n, 256, 4), d->batch);
+      k_gemm_reduce<<<rgrid, 256, 0, ESGD_STREAM(stream)>>>(*d, splits);
+    }
   }
   return check_launch("esgd_gemm_f32");
 }
